@@ -1,0 +1,422 @@
+"""B200 bench for the ELL-WARP SpMV + Jacobi PCG path (BASELINE.json).
+
+Default (N=1): fp64 SpMV effective bandwidth on config 2 (3-DOF linear
+elasticity tet mesh, 1,975,509 rows, 87.3M nonzeros) through the prepared
+K1 kernel, device-resident inputs. One JSON line on stdout (rank 0).
+
+  value      paper-effective bandwidth 20*nnz / t (csr.cpp:92)
+  roofline   algorithmic bytes 12*nnz + 8*nrows + 8*ncols of the dominant
+             kernel (k1_kernel) / its CUDA-event time vs MEASURED_PEAKS hbm
+  e2e        same metric through ew_kernel_apply with pinned HOST buffers,
+             H2D x + D2H y inside the timed region
+  cpu_baseline  the reference's own prepare_kernel("k1").apply, compiled
+             from its sources (oracle/_ref), single thread, on this host
+
+--workload cg: Jacobi PCG iterations/s on config 4 (ventricle-like mesh,
+5M rows, random renumbering), k1rs in permuted space, 1000 iterations.
+
+--impl reference: the reference's CPU implementation on the same config and
+metric (oracle/_ref, 1 thread: the reference has no threading).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(name="fp64 SpMV, 3D linear-tet Laplacian 64^3 nodes (262,144 rows)", gen="laplacian_box",
+               dims=(63, 63, 63)),
+    "c2": dict(name="fp64 SpMV, 3-DOF linear-elasticity tet mesh 87^3 nodes (1,975,509 rows)",
+               gen="elasticity_box", dims=(86, 86, 86)),
+    "c4": dict(name="Jacobi PCG 1000 it, jittered+renumbered tet ventricle-like mesh 171^3 nodes (5,000,211 rows)",
+               gen="ventricle_box", dims=(170, 170, 170)),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def build_matrix(cfg_key, scale=1.0):
+    from paper_1501_00324_b200 import workloads as W
+
+    c = CONFIGS[cfg_key]
+    dims = tuple(max(2, int(round(d * scale))) for d in c["dims"])
+    t = time.time()
+    n, nc, ro, ci, v = getattr(W, c["gen"])(*dims)
+    log(f"[bench] {cfg_key} {dims}: {n} rows, {ro[-1]} nnz, generated in {time.time() - t:.1f}s")
+    return n, nc, ro, ci, v
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.thread.join(1)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, val in zip(names, r[4:8]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(n_gpus):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference (oracle/_ref) on a bounded sample
+# ---------------------------------------------------------------------------
+def reference_spmv_rate(n, nc, ro, ci, v, kernel="k1", budget_s=15.0, max_calls=50):
+    from oracle.oracle import Csr, Reference
+
+    F = Reference()
+    m = Csr.make(n, nc, ro, ci, v)
+    x = np.random.default_rng(1).uniform(0.1, 1.0, nc)
+    y = np.empty(n)
+    t0 = time.perf_counter()
+    h = F.prepare(kernel, m)
+    t_prep = time.perf_counter() - t0
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_calls and (time.perf_counter() - t_start) < budget_s:
+        t = time.perf_counter()
+        F.run(h, x, y)
+        times.append(time.perf_counter() - t)
+    F.free_prepared(h)
+    med = float(np.median(times))
+    return med, len(times), t_prep
+
+
+def reference_cg_rate(n, nc, ro, ci, v, iters):
+    from oracle.oracle import Csr, Reference
+
+    F = Reference()
+    m = Csr.make(n, nc, ro, ci, v)
+    b = F.spmv_csr(m, np.ones(nc))
+    t = time.perf_counter()
+    res = F.cg("csr_ref", m, b, tol=1e-300, max_iterations=iters)
+    dt = time.perf_counter() - t
+    return res.iterations / dt, res.iterations, dt
+
+
+# ---------------------------------------------------------------------------
+# GPU arms
+# ---------------------------------------------------------------------------
+def run_spmv(args, rank, world, local):
+    import torch
+
+    from paper_1501_00324_b200 import capi
+
+    hbm, peak_src = peaks()
+    n, nc, ro, ci, v = build_matrix(args.config, args.scale)
+    nnz = int(ro[-1])
+    t = time.time()
+    a = capi.Csr(n, nc, ro, ci, v)
+    k = capi.Kernel(args.kernel, a, threshold=args.threshold)
+    torch.cuda.synchronize()
+    t_prepare = time.time() - t
+    log(f"[bench] rank {rank}: upload+validate+prepare({args.kernel}) {t_prepare:.2f}s, "
+        f"stored_slots {k.stored_slots} ({k.stored_slots - nnz} padded)")
+    x = torch.tensor(np.random.default_rng(1).uniform(0.1, 1.0, nc), device="cuda")
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    apply = k.apply_permuted if args.permuted else k.apply
+
+    # warm-up, then exactly K timed steps between barriers + syncs
+    for _ in range(args.warmup):
+        apply(x, y, stream=stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = capi.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            apply(x, y, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = capi.launch_count() - l0
+    barrier(world)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+
+    eff_bytes = 20 * nnz
+    alg_bytes = 12 * nnz + 8 * n + 8 * nc
+    value = world * eff_bytes / (ms * 1e-3) / 1e9
+    # dominant kernel: one k1_kernel launch per step (gather kernels only for
+    # r/rs apply); its per-launch time is the step time when launches == steps
+    kern_ms = ms_local if launches == args.steps else None
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms else None
+
+    # end-to-end through the C ABI with pinned host buffers
+    xh = torch.empty(nc, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x.cpu())
+    yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xn, yn = xh.numpy(), yh.numpy()
+    k_e2e = max(3, min(args.steps, 50))
+    for _ in range(2):
+        apply(xn, yn)
+    barrier(world)
+    t = time.perf_counter()
+    for _ in range(k_e2e):
+        apply(xn, yn)
+    e2e_ms = max_over_ranks((time.perf_counter() - t) * 1e3 / k_e2e, world)
+    e2e_val = world * eff_bytes / (e2e_ms * 1e-3) / 1e9
+
+    out = {
+        "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded structured tet mesh, values from P1 elasticity element matrices)",
+        "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel,
+                   "permuted": bool(args.permuted), "nrows": n, "nnz": nnz, "stored_slots": k.stored_slots,
+                   "per_rank": "independent copy per GPU" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (%.2f GB algorithmic bytes vs 126 MB L2)" % (alg_bytes / 1e9)
+                   if alg_bytes > 3 * 126e6 else "L2-resident working set: warm-L2 number"},
+        "effective_pct_of_hbm": round(100 * value / world / hbm, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
+                     "kernel": "k1_kernel" if args.kernel.startswith("k1") else "k2_kernel",
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
+                "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "prepare_s": round(t_prepare, 3),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        med, calls, t_prep = reference_spmv_rate(n, nc, ro, ci, v, kernel=args.kernel)
+        out["cpu_baseline"] = {"value": round(eff_bytes / med / 1e9, 3), "unit": "GB/s", "cores": 1,
+                               "kind": "reference",
+                               "sample": f"full {args.config} matrix, median of {calls} prepare_kernel('"
+                                         f"{args.kernel}').apply calls (oracle/_ref, 1 thread); "
+                                         f"CPU layout build {t_prep:.1f}s"}
+    return out
+
+
+def run_cg(args, rank, world, local):
+    import torch
+
+    from paper_1501_00324_b200 import capi
+
+    hbm, peak_src = peaks()
+    n, nc, ro, ci, v = build_matrix(args.config, args.scale)
+    nnz = int(ro[-1])
+    a = capi.Csr(n, nc, ro, ci, v)
+    k = capi.Kernel(args.kernel, a, threshold=args.threshold)
+    diag = a.extract_diagonal()
+    b = a.spmv(np.ones(nc))  # b = A * 1 (ellwarp_cli.cpp:192-195)
+    bd = torch.tensor(b, device="cuda")
+    dd = torch.tensor(diag, device="cuda")
+    iters = args.iterations
+    for _ in range(args.warmup):
+        k.cg_solve(bd, dd, tol=1e-300, max_iterations=20, permuted=args.permuted)
+    torch.cuda.synchronize()
+    barrier(world)
+    l0 = capi.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        tot = 0
+        for _ in range(args.steps):
+            res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+            tot += res.iterations
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = capi.launch_count() - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    it_s = world * iters / (ms * 1e-3)
+    b_it = 12 * nnz + 104 * n + (12 * nnz + 24 * n) / 50
+    out = {
+        "metric": "CG iterations/s", "value": round(it_s, 2), "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
+                   "iterations_per_step": iters, "nrows": n, "nnz": nnz},
+        "roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
+                     "traffic": None, "algorithmic_bytes_per_iteration": b_it},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, its, dt = reference_cg_rate(n, nc, ro, ci, v, iters=max(2, args.cpu_cg_iters))
+        out["cpu_baseline"] = {"value": round(rate, 3), "unit": "it/s", "cores": 1, "kind": "reference",
+                               "sample": f"cg_solve(csr_ref) {its} iterations on the full matrix "
+                                         f"({dt:.1f}s, oracle/_ref, 1 thread)"}
+    return out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    n, nc, ro, ci, v = build_matrix(args.config, args.scale)
+    nnz = int(ro[-1])
+    cores = 1
+    if args.workload == "cg":
+        rate, its, dt = reference_cg_rate(n, nc, ro, ci, v, iters=max(2, args.cpu_cg_iters))
+        return {"impl": "reference", "metric": "CG iterations/s", "value": round(rate, 3), "unit": "it/s",
+                "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": True,
+                "config": {"workload": CONFIGS[args.config]["name"]},
+                "cpu_baseline": {"kind": "reference", "cores": cores, "value": round(rate, 3),
+                                 "sample": f"{its} iterations cg_solve(csr_ref)"},
+                "e2e": {"value": round(rate, 3), "unit": "it/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+    med, calls, t_prep = reference_spmv_rate(n, nc, ro, ci, v, kernel=args.kernel,
+                                             budget_s=min(60.0, 3.0 * max(1, args.steps)),
+                                             max_calls=max(args.steps, 1))
+    val = 20 * nnz / med / 1e9
+    return {"impl": "reference", "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)", "value": round(val, 3),
+            "unit": "GB/s", "n_gpus": world, "steps": calls, "warmup": 0, "ms_per_step": round(med * 1e3, 3),
+            "higher_is_better": True, "dtype": "f64",
+            "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel},
+            "cpu_baseline": {"kind": "reference", "cores": cores, "value": round(val, 3), "unit": "GB/s",
+                             "sample": f"median of {calls} prepare_kernel('{args.kernel}').apply calls, full matrix "
+                                       "(oracle/_ref compiled from the reference sources; single-threaded "
+                                       "by construction)"},
+            "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=["spmv", "cg"], default="spmv")
+    p.add_argument("--config", default=None)
+    p.add_argument("--kernel", default=None)
+    p.add_argument("--threshold", type=int, default=0)
+    p.add_argument("--permuted", action="store_true")
+    p.add_argument("--scale", type=float, default=1.0, help="mesh edge scale (tests only)")
+    p.add_argument("--iterations", type=int, default=1000)
+    p.add_argument("--cpu-cg-iters", type=int, default=20)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.config is None:
+        args.config = "c4" if args.workload == "cg" else "c2"
+    if args.kernel is None:
+        args.kernel = "k1rs" if args.workload == "cg" else "k1"
+    if args.workload == "cg":
+        args.permuted = args.permuted or args.kernel.endswith(("r", "rs"))
+    if args.steps is None:
+        args.steps = 3 if args.workload == "cg" else 2000
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        out = run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    rank, world, local = dist_init(args.gpus)
+    out = run_spmv(args, rank, world, local) if args.workload == "spmv" else run_cg(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

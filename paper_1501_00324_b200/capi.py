@@ -1,0 +1,550 @@
+"""ctypes binding of the C ABI in include/ellwarp_b200.h.
+
+This is the boundary the parity tests and bench.py call through. It loads the
+in-tree ``lib/libellwarp_b200.so`` and raises immediately when it is missing:
+there is no CPU fallback anywhere in this package.
+
+Status codes become the reference's exceptions (types.hpp:16-18, cg.hpp:28-30):
+EW_INVALID_ARGUMENT -> ValueError (Python's std::invalid_argument, as pybind11
+maps it), EW_CG_DIVERGENCE -> CgDivergenceError, EW_UNSUPPORTED ->
+UnsupportedError, EW_CUDA / EW_OUT_OF_MEMORY -> DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libellwarp_b200.so")
+
+EW_OK, EW_INVALID_ARGUMENT, EW_CG_DIVERGENCE, EW_UNSUPPORTED, EW_CUDA, EW_OUT_OF_MEMORY = range(6)
+EW_MEM_HOST, EW_MEM_DEVICE = 0, 1
+EW_LAYOUT_K1, EW_LAYOUT_K2 = 1, 2
+
+
+class CgDivergenceError(RuntimeError):
+    """ellwarp::CgDivergenceError (cg.hpp:28-30)."""
+
+
+class UnsupportedError(RuntimeError):
+    """Input the device path rejects (EW_UNSUPPORTED)."""
+
+
+class DeviceError(RuntimeError):
+    """A CUDA failure inside the library (EW_CUDA / EW_OUT_OF_MEMORY)."""
+
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class WarpConfig(C.Structure):
+    """WarpModelConfig (warp_model.hpp:16-25)."""
+
+    _fields_ = [("warp_size", C.c_int32), ("block_size", C.c_int32), ("segment_bytes", C.c_int32),
+                ("align_warp_offsets", C.c_int32), ("ideal_cache", C.c_int32),
+                ("cache_lines", C.c_int32)]
+
+    @staticmethod
+    def make(warp_size=32, block_size=None, segment_bytes=128, align=True):
+        # the reference binding's make_config: block_size = max(32, ws) (module.cpp:16-26)
+        bs = block_size if block_size is not None else max(32, warp_size)
+        return WarpConfig(warp_size, bs, segment_bytes, 1 if align else 0, 0, 64)
+
+
+class KernelOptions(C.Structure):
+    _fields_ = [("k2_threshold", C.c_int64), ("hyb_k_ell", C.c_int64)]
+
+
+class CgConfig(C.Structure):
+    _fields_ = [("rel_tolerance", C.c_double), ("max_iterations", C.c_int64), ("jacobi", C.c_int32),
+                ("recompute_interval", C.c_int64), ("divergence_limit", C.c_double)]
+
+
+class CgResultC(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("converged", C.c_int32), ("spmv_calls", C.c_int64),
+                ("history_len", C.c_int64)]
+
+
+class LayoutInfo(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("warp_size", C.c_int32), ("row_major", C.c_int32),
+                ("sorted", C.c_int32), ("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
+                ("nwarps", C.c_int64), ("nslots", C.c_int64), ("stored_slots", C.c_int64),
+                ("threshold", C.c_int64), ("device_bytes", C.c_int64)]
+
+
+class LayoutArrays(C.Structure):
+    _fields_ = [("values", _f64p), ("col_indices", _i64p), ("warp_offset", _i64p), ("maxrows", _i64p),
+                ("rows_in_warp", _i64p), ("reduction", _i64p), ("rows_offset_warp", _i64p),
+                ("forward", _i64p), ("inverse", _i64p), ("sorted_row_length", _i64p)]
+
+
+class LayoutDesc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("warp_size", C.c_int32), ("row_major", C.c_int32),
+                ("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64), ("nwarps", C.c_int64),
+                ("nslots", C.c_int64), ("threshold", C.c_int64), ("values", _f64p),
+                ("col_indices", _i64p), ("warp_offset", _i64p), ("maxrows", _i64p),
+                ("rows_in_warp", _i64p), ("reduction", _i64p), ("rows_offset_warp", _i64p),
+                ("forward", _i64p), ("sorted_row_length", _i64p)]
+
+
+class KernelInfo(C.Structure):
+    _fields_ = [("id", C.c_char * 16), ("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
+                ("stored_slots", C.c_int64), ("nwarps", C.c_int64), ("has_perm", C.c_int32),
+                ("layout_kind", C.c_int32), ("device_bytes", C.c_int64)]
+
+
+OPERATOR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+# every symbol include/ellwarp_b200.h declares, with its ctypes signature
+_SIGS = {
+    "ew_last_error": (C.c_char_p, []),
+    "ew_status_string": (C.c_char_p, [C.c_int]),
+    "ew_abi_version": (C.c_int32, []),
+    "ew_kernel_id_count": (C.c_int32, []),
+    "ew_kernel_id": (C.c_char_p, [C.c_int32]),
+    "ew_kernel_id_supported": (C.c_int32, [C.c_char_p]),
+    "ew_launch_count": (C.c_int64, []),
+    "ew_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_int, _vp,
+                                C.POINTER(_vp)]),
+    "ew_csr_destroy": (C.c_int, [_vp]),
+    "ew_csr_shape": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
+    "ew_csr_export": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "ew_csr_update_values": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ew_csr_spmv": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int, _vp]),
+    "ew_csr_extract_diagonal": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ew_sort_rows_desc": (C.c_int, [_vp, _vp, _vp]),
+    "ew_reorder": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), _vp]),
+    "ew_compute_k2_lanes": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _i64p]),
+    "ew_layout_build": (C.c_int, [_vp, C.c_int32, C.POINTER(WarpConfig), C.c_int64, C.c_int32, C.c_int32,
+                                  C.POINTER(_vp)]),
+    "ew_layout_import": (C.c_int, [C.POINTER(LayoutDesc), C.POINTER(_vp)]),
+    "ew_layout_destroy": (C.c_int, [_vp]),
+    "ew_layout_get_info": (C.c_int, [_vp, C.POINTER(LayoutInfo)]),
+    "ew_layout_export": (C.c_int, [_vp, C.POINTER(LayoutArrays)]),
+    "ew_layout_value_slot_map": (C.c_int, [_vp, _vp, _vp]),
+    "ew_layout_refresh_values": (C.c_int, [_vp, _vp, _vp]),
+    "ew_layout_dump": (C.c_int, [_vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ew_layout_spmv": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int32, C.c_int, _vp]),
+    "ew_kernel_prepare": (C.c_int, [C.c_char_p, _vp, C.POINTER(WarpConfig), C.POINTER(KernelOptions),
+                                    C.POINTER(_vp)]),
+    "ew_kernel_destroy": (C.c_int, [_vp]),
+    "ew_kernel_get_info": (C.c_int, [_vp, C.POINTER(KernelInfo)]),
+    "ew_kernel_get_perm": (C.c_int, [_vp, _vp, _vp]),
+    "ew_kernel_get_layout": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ew_kernel_apply": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int, _vp]),
+    "ew_kernel_apply_permuted": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int, _vp]),
+    "ew_kernel_refresh_values": (C.c_int, [_vp, _vp, _vp]),
+    "ew_cg_solve": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.POINTER(CgConfig), C.c_int, _vp, _vp,
+                              C.POINTER(CgResultC), _vp]),
+    "ew_cg_solve_permuted": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.POINTER(CgConfig), C.c_int, _vp, _vp,
+                                       C.POINTER(CgResultC), _vp]),
+    "ew_cg_solve_operator": (C.c_int, [OPERATOR_FN, _vp, C.c_int, _vp, _vp, C.c_int64, C.POINTER(CgConfig),
+                                       C.c_int, _vp, _vp, C.POINTER(CgResultC), _vp]),
+    "ew_compute_alpha": (C.c_int, [C.c_double, C.c_double, C.c_double, _i64p, C.POINTER(C.c_int32)]),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded C library; raises if the CUDA build is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def declared_symbols():
+    return list(_SIGS)
+
+
+def check(status):
+    if status == EW_OK:
+        return
+    msg = lib().ew_last_error().decode(errors="replace")
+    if status == EW_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == EW_CG_DIVERGENCE:
+        raise CgDivergenceError(msg)
+    if status == EW_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise DeviceError(f"{msg} (status {status})")
+
+
+def kernel_ids():
+    L = lib()
+    return [L.ew_kernel_id(i).decode() for i in range(L.ew_kernel_id_count())]
+
+
+def launch_count():
+    return int(lib().ew_launch_count())
+
+
+# --------------------------------------------------------------------------
+# buffers: numpy (host) or anything with data_ptr() (torch CUDA tensors)
+# --------------------------------------------------------------------------
+def _host(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(a.ctypes.data)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def _mem_of(a):
+    return EW_MEM_DEVICE if hasattr(a, "data_ptr") else EW_MEM_HOST
+
+
+class Csr:
+    """Device-resident SparseCsr (ew_csr)."""
+
+    def __init__(self, nrows, ncols, row_offsets, col_indices, values, stream=None):
+        ro = row_offsets if hasattr(row_offsets, "data_ptr") else _host(row_offsets, np.int64)
+        ci = col_indices if hasattr(col_indices, "data_ptr") else _host(col_indices, np.int64)
+        v = values if hasattr(values, "data_ptr") else _host(values, np.float64)
+        nnz = ci.numel() if hasattr(ci, "numel") else ci.size
+        nv = v.numel() if hasattr(v, "numel") else v.size
+        nro = ro.numel() if hasattr(ro, "numel") else ro.size
+        if nv != nnz:
+            raise ValueError("values/col_indices length mismatch")
+        h = C.c_void_p()
+        check(lib().ew_csr_create(int(nrows), int(ncols), int(nro), _ptr(ro), int(nnz), _ptr(ci), _ptr(v),
+                                  _mem_of(ro), _stream_ptr(stream), C.byref(h)))
+        self.h = h
+        self.nrows, self.ncols, self.nnz = int(nrows), int(ncols), int(nnz)
+
+    @staticmethod
+    def from_oracle(m):
+        return Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+
+    @staticmethod
+    def _wrap(h):
+        obj = Csr.__new__(Csr)
+        obj.h = h
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ew_csr_shape(h, C.byref(a), C.byref(b), C.byref(c)))
+        obj.nrows, obj.ncols, obj.nnz = a.value, b.value, c.value
+        return obj
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.ew_csr_destroy(h)
+            self.h = None
+
+    def export(self):
+        ro = np.empty(self.nrows + 1, np.int64)
+        ci = np.empty(self.nnz, np.int64)
+        v = np.empty(self.nnz, np.float64)
+        check(lib().ew_csr_export(self.h, _ptr(ro), _ptr(ci), _ptr(v)))
+        return ro, ci, v
+
+    def update_values(self, values, stream=None):
+        v = values if hasattr(values, "data_ptr") else _host(values, np.float64)
+        check(lib().ew_csr_update_values(self.h, _ptr(v), _mem_of(v), _stream_ptr(stream)))
+
+    def spmv(self, x, y=None, stream=None):
+        """spmv_csr_reference on the device (bit-identical)."""
+        return _apply(lambda xp, nx, yp, ny, mem, s: lib().ew_csr_spmv(self.h, xp, nx, yp, ny, mem, s),
+                      x, y, self.ncols, self.nrows, stream)
+
+    def extract_diagonal(self):
+        d = np.empty(self.nrows, np.float64)
+        check(lib().ew_csr_extract_diagonal(self.h, _ptr(d), EW_MEM_HOST, None))
+        return d
+
+    def sort_rows_desc(self):
+        fwd = np.empty(self.nrows, np.int64)
+        inv = np.empty(self.nrows, np.int64)
+        check(lib().ew_sort_rows_desc(self.h, _ptr(fwd), _ptr(inv)))
+        return fwd, inv
+
+    def reorder(self, sort_within_rows=False):
+        h = C.c_void_p()
+        fwd = np.empty(self.nrows, np.int64)
+        check(lib().ew_reorder(self.h, 1 if sort_within_rows else 0, C.byref(h), _ptr(fwd)))
+        return Csr._wrap(h), fwd
+
+
+def _apply(fn, x, y, nx, ny, stream):
+    if hasattr(x, "data_ptr"):
+        if y is None:
+            import torch
+
+            y = torch.empty(ny, dtype=torch.float64, device=x.device)
+        check(fn(_ptr(x), nx, _ptr(y), ny, EW_MEM_DEVICE, _stream_ptr(stream)))
+        return y
+    xh = _host(x, np.float64)
+    if xh.size != nx:
+        # let the library report the reference's dimension error
+        pass
+    yh = np.empty(ny, np.float64) if y is None else y
+    check(fn(_ptr(xh), xh.size, _ptr(yh), ny, EW_MEM_HOST, _stream_ptr(stream)))
+    return yh
+
+
+def compute_k2_lanes(nnz_row, threshold, warp_size=32):
+    out = C.c_int64()
+    check(lib().ew_compute_k2_lanes(int(nnz_row), int(threshold), int(warp_size), C.byref(out)))
+    return out.value
+
+
+@dataclass
+class LayoutExport:
+    kind: str
+    warp_size: int
+    nrows: int
+    ncols: int
+    nnz: int
+    threshold: int
+    stored_slots: int
+    values: np.ndarray
+    col_indices: np.ndarray
+    warp_offset: np.ndarray
+    maxrows: np.ndarray
+    rows_in_warp: np.ndarray
+    forward: np.ndarray
+    inverse: np.ndarray
+    sorted_row_length: np.ndarray
+    reduction: np.ndarray | None = None
+    rows_offset_warp: np.ndarray | None = None
+
+    @property
+    def nwarps(self):
+        return int(self.warp_offset.size)
+
+    @property
+    def padded_slots(self):
+        return self.stored_slots - self.nnz
+
+
+class Layout:
+    """Device WarpLayoutK1 / WarpLayoutK2 (ew_layout)."""
+
+    def __init__(self, h, owner=None):
+        self.h = h
+        self._owner = owner  # a Kernel owns its layout
+
+    @staticmethod
+    def build(csr: Csr, kind="k1", warp_size=32, threshold=0, segment_bytes=128, align=True,
+              sort_rows=True, row_major=False):
+        cfg = WarpConfig.make(warp_size, segment_bytes=segment_bytes, align=align)
+        h = C.c_void_p()
+        check(lib().ew_layout_build(csr.h, EW_LAYOUT_K1 if kind == "k1" else EW_LAYOUT_K2, C.byref(cfg),
+                                    int(threshold), 1 if sort_rows else 0, 1 if row_major else 0, C.byref(h)))
+        return Layout(h)
+
+    @staticmethod
+    def import_arrays(kind, warp_size, nrows, ncols, nnz, values, col_indices, warp_offset, maxrows,
+                      rows_in_warp, forward, sorted_row_length, reduction=None, rows_offset_warp=None,
+                      threshold=0, row_major=False):
+        keep = [_host(values, np.float64), _host(col_indices, np.int64), _host(warp_offset, np.int64),
+                _host(maxrows, np.int64), _host(rows_in_warp, np.int64), _host(forward, np.int64),
+                _host(sorted_row_length, np.int64)]
+        red = _host(reduction, np.int64) if reduction is not None else None
+        row = _host(rows_offset_warp, np.int64) if rows_offset_warp is not None else None
+        d = LayoutDesc(EW_LAYOUT_K1 if kind == "k1" else EW_LAYOUT_K2, warp_size, 1 if row_major else 0,
+                       nrows, ncols, nnz, keep[2].size, keep[0].size, threshold,
+                       keep[0].ctypes.data_as(_f64p), keep[1].ctypes.data_as(_i64p),
+                       keep[2].ctypes.data_as(_i64p), keep[3].ctypes.data_as(_i64p),
+                       keep[4].ctypes.data_as(_i64p), red.ctypes.data_as(_i64p) if red is not None else None,
+                       row.ctypes.data_as(_i64p) if row is not None else None,
+                       keep[5].ctypes.data_as(_i64p), keep[6].ctypes.data_as(_i64p))
+        h = C.c_void_p()
+        check(lib().ew_layout_import(C.byref(d), C.byref(h)))
+        return Layout(h)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and self._owner is None and _lib is not None:
+            _lib.ew_layout_destroy(h)
+            self.h = None
+
+    def info(self):
+        i = LayoutInfo()
+        check(lib().ew_layout_get_info(self.h, C.byref(i)))
+        return i
+
+    def export(self) -> LayoutExport:
+        i = self.info()
+        nw, ns, n = i.nwarps, i.nslots, i.nrows
+        arr = dict(values=np.empty(ns, np.float64), col_indices=np.empty(ns, np.int64),
+                   warp_offset=np.empty(nw, np.int64), maxrows=np.empty(nw, np.int64),
+                   rows_in_warp=np.empty(nw, np.int64), forward=np.empty(n, np.int64),
+                   inverse=np.empty(n, np.int64), sorted_row_length=np.empty(n, np.int64))
+        if i.kind == EW_LAYOUT_K2:
+            arr["reduction"] = np.empty(nw, np.int64)
+            arr["rows_offset_warp"] = np.empty(nw, np.int64)
+        a = LayoutArrays()
+        for k, v in arr.items():
+            setattr(a, k, v.ctypes.data_as(_f64p if v.dtype == np.float64 else _i64p))
+        check(lib().ew_layout_export(self.h, C.byref(a)))
+        return LayoutExport(kind="k1" if i.kind == EW_LAYOUT_K1 else "k2", warp_size=i.warp_size,
+                            nrows=n, ncols=i.ncols, nnz=i.nnz, threshold=i.threshold,
+                            stored_slots=i.stored_slots, **arr)
+
+    def value_slot_map(self, csr: Csr):
+        out = np.empty(csr.nnz, np.int64)
+        check(lib().ew_layout_value_slot_map(self.h, csr.h, _ptr(out)))
+        return out
+
+    def refresh_values(self, csr: Csr, stream=None):
+        check(lib().ew_layout_refresh_values(self.h, csr.h, _stream_ptr(stream)))
+
+    def dump(self):
+        n = C.c_size_t()
+        check(lib().ew_layout_dump(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().ew_layout_dump(self.h, buf, n.value, C.byref(n)))
+        return buf.value.decode()
+
+    def spmv(self, x, y=None, scatter=True, stream=None):
+        i = self.info()
+        return _apply(lambda xp, nx, yp, ny, mem, s: lib().ew_layout_spmv(self.h, xp, nx, yp, ny,
+                                                                           1 if scatter else 0, mem, s),
+                      x, y, i.ncols, i.nrows, stream)
+
+
+@dataclass
+class CgResult:
+    solution: object
+    iterations: int
+    residual_history: np.ndarray
+    converged: bool
+    spmv_calls: int
+
+
+class Kernel:
+    """PreparedKernel (kernels.hpp:16-23) over device data (ew_kernel)."""
+
+    def __init__(self, kernel_id, csr: Csr, warp_size=32, threshold=0, segment_bytes=128, align=True,
+                 block_size=None, hyb_k_ell=-1):
+        cfg = WarpConfig.make(warp_size, block_size=block_size, segment_bytes=segment_bytes, align=align)
+        opts = KernelOptions(int(threshold), int(hyb_k_ell))
+        h = C.c_void_p()
+        check(lib().ew_kernel_prepare(kernel_id.encode(), csr.h, C.byref(cfg), C.byref(opts), C.byref(h)))
+        self.h = h
+        self.id = kernel_id
+        info = self.info()
+        self.nrows, self.ncols, self.nnz = info.nrows, info.ncols, info.nnz
+        self.stored_slots = info.stored_slots
+        self.has_perm = bool(info.has_perm)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.ew_kernel_destroy(h)
+            self.h = None
+
+    def info(self):
+        i = KernelInfo()
+        check(lib().ew_kernel_get_info(self.h, C.byref(i)))
+        return i
+
+    def perm(self):
+        fwd = np.empty(self.nrows, np.int64)
+        inv = np.empty(self.nrows, np.int64)
+        check(lib().ew_kernel_get_perm(self.h, _ptr(fwd), _ptr(inv)))
+        return fwd, inv
+
+    def layout(self):
+        h = C.c_void_p()
+        check(lib().ew_kernel_get_layout(self.h, C.byref(h)))
+        return Layout(h, owner=self) if h.value else None
+
+    def apply(self, x, y=None, stream=None):
+        return _apply(lambda xp, nx, yp, ny, mem, s: lib().ew_kernel_apply(self.h, xp, nx, yp, ny, mem, s),
+                      x, y, self.ncols, self.nrows, stream)
+
+    def apply_permuted(self, x, y=None, stream=None):
+        return _apply(lambda xp, nx, yp, ny, mem, s: lib().ew_kernel_apply_permuted(self.h, xp, nx, yp, ny,
+                                                                                    mem, s),
+                      x, y, self.ncols, self.nrows, stream)
+
+    def refresh_values(self, csr: Csr, stream=None):
+        check(lib().ew_kernel_refresh_values(self.h, csr.h, _stream_ptr(stream)))
+
+    def cg_solve(self, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=True, recompute_interval=50,
+                 divergence_limit=1e6, permuted=False, x=None, stream=None):
+        """cg_solve (or cg_solve_permuted) with this kernel as the operator."""
+        cfg = CgConfig(float(tol), int(max_iterations), 1 if jacobi else 0, int(recompute_interval),
+                       float(divergence_limit))
+        dev = hasattr(b, "data_ptr")
+        if dev:
+            import torch
+
+            x = torch.empty_like(b) if x is None else x
+        else:
+            b = _host(b, np.float64)
+            diag = _host(diag, np.float64) if diag is not None else None
+            x = np.empty(b.size, np.float64)
+        n = b.numel() if dev else b.size
+        hist = np.empty(int(max_iterations) + 1, np.float64)
+        res = CgResultC()
+        fn = lib().ew_cg_solve_permuted if permuted else lib().ew_cg_solve
+        check(fn(self.h, _ptr(b), _ptr(diag), int(n), C.byref(cfg), EW_MEM_DEVICE if dev else EW_MEM_HOST,
+                 _ptr(x), _ptr(hist), C.byref(res), _stream_ptr(stream)))
+        return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
+                        int(res.spmv_calls))
+
+
+def cg_solve_operator(op, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=True, recompute_interval=50,
+                      divergence_limit=1e6):
+    """cg_solve with a Python operator ``op(x: np.ndarray) -> np.ndarray`` (the
+    reference's SpmvFn closure, cg.hpp:32); vector work and dots run on the
+    device, x / y are staged through host buffers around each call."""
+    b = _host(b, np.float64)
+    diag = _host(diag, np.float64) if diag is not None else None
+    n = b.size
+
+    def cb(ctx, xp, yp, stream):
+        try:
+            xh = np.ctypeslib.as_array(C.cast(xp, _f64p), shape=(n,))
+            yh = np.ctypeslib.as_array(C.cast(yp, _f64p), shape=(n,))
+            yh[:] = np.asarray(op(xh.copy()), np.float64)
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the C side as a status
+            return EW_INVALID_ARGUMENT
+
+    fn = OPERATOR_FN(cb)
+    cfg = CgConfig(float(tol), int(max_iterations), 1 if jacobi else 0, int(recompute_interval),
+                   float(divergence_limit))
+    x = np.empty(n, np.float64)
+    hist = np.empty(int(max_iterations) + 1, np.float64)
+    res = CgResultC()
+    check(lib().ew_cg_solve_operator(fn, None, EW_MEM_HOST, _ptr(b), _ptr(diag), n, C.byref(cfg),
+                                     EW_MEM_HOST, _ptr(x), _ptr(hist), C.byref(res), None))
+    return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
+                    int(res.spmv_calls))
+
+
+def compute_alpha(t_reorder, t_kernel, t_base):
+    a = C.c_int64()
+    f = C.c_int32()
+    check(lib().ew_compute_alpha(float(t_reorder), float(t_kernel), float(t_base), C.byref(a), C.byref(f)))
+    return a.value if f.value else None

@@ -1,0 +1,612 @@
+// The extern "C" boundary (include/ellwarp_b200.h). Each entry point catches
+// every C++ exception and turns it into a status + thread-local message.
+#include <cstring>
+#include <sstream>
+
+#include "ew_internal.cuh"
+
+struct ew_csr_t {
+    std::shared_ptr<ew::CsrData> d;
+};
+struct ew_layout_t {
+    std::shared_ptr<ew::LayoutData> d;
+};
+struct ew_kernel_t {
+    std::shared_ptr<ew::KernelData> d;
+    ew_layout_t layout_view;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+ew_status guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return EW_OK;
+    } catch (const ew::Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = "host allocation failed";
+        return EW_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return EW_CUDA;
+    }
+}
+
+const char* const kIds[] = {"csr_ref", "csr_vector", "coo", "ell",  "hyb", "k1",
+                            "k1r",     "k1rs",       "k2",  "k2r", "k2rs"};
+constexpr int kNumIds = 11;
+
+int id_support(const std::string& id) {
+    for (int i = 0; i < kNumIds; ++i) {
+        if (id == kIds[i]) {
+            if (id == "csr_vector" || id == "coo" || id == "ell" || id == "hyb") return 0;
+            return 1;
+        }
+    }
+    return -1;
+}
+
+ew_warp_config default_config() { return ew_warp_config{32, 128, 128, 1, 0, 64}; }
+
+// Runs `op(x_dev, y_dev)` for host or device buffers.
+template <typename Op>
+void with_io(const double* x, int64_t nx, double* y, int64_t ny, ew_mem_kind mem, cudaStream_t s,
+             Op&& op) {
+    if (mem == EW_MEM_DEVICE) {
+        op(x, y);
+        ew::launched("with_io(device)");  // surfaces async launch errors
+        return;
+    }
+    ew::Scratch<double> xd(nx, s), yd(ny, s);
+    if (nx) EW_CUDA_CHECK(cudaMemcpyAsync(xd.get(), x, nx * sizeof(double), cudaMemcpyHostToDevice, s));
+    op(xd.get(), yd.get());
+    if (ny) EW_CUDA_CHECK(cudaMemcpyAsync(y, yd.get(), ny * sizeof(double), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void widen(const ew::DevBuf<int32_t>& src, int64_t* dst, size_t n) {
+    if (!dst || n == 0) return;
+    std::vector<int32_t> h(n);
+    EW_CUDA_CHECK(cudaMemcpy(h.data(), src.get(), n * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) dst[i] = h[i];
+}
+
+void check_handle(const void* h, const char* what) {
+    if (!h) throw ew::Error(EW_INVALID_ARGUMENT, std::string(what) + " handle is null");
+}
+
+std::string dump(const ew::LayoutData& l) {
+    // dump_layout (warp_layout.cpp:185-207), byte-identical text
+    const size_t nw = static_cast<size_t>(l.nwarps);
+    std::vector<int64_t> off(nw), mx(nw), riw(nw), red(nw, 1), row(nw);
+    if (nw) {
+        EW_CUDA_CHECK(cudaMemcpy(off.data(), l.warp_offset.get(), nw * 8, cudaMemcpyDeviceToHost));
+        widen(l.maxrows, mx.data(), nw);
+        widen(l.rows_in_warp, riw.data(), nw);
+        if (l.kind == EW_LAYOUT_K2) {
+            widen(l.reduction, red.data(), nw);
+            widen(l.rows_offset_warp, row.data(), nw);
+        }
+    }
+    std::ostringstream os;
+    if (l.kind == EW_LAYOUT_K1) {
+        os << "k1 warp_size=" << l.ws << " nrows=" << l.nrows << " nnz=" << l.nnz << " nwarps=" << nw
+           << "\n";
+        for (size_t w = 0; w < nw; ++w) {
+            const int64_t first = static_cast<int64_t>(w) * l.ws;
+            os << "warp " << w << ": offset=" << off[w] << " maxrows=" << mx[w] << " reduction=1 rows=["
+               << first << "," << first + riw[w] << ")\n";
+        }
+    } else {
+        os << "k2 warp_size=" << l.ws << " nrows=" << l.nrows << " nnz=" << l.nnz
+           << " threshold=" << l.threshold << " nwarps=" << nw << "\n";
+        for (size_t w = 0; w < nw; ++w) {
+            os << "warp " << w << ": offset=" << off[w] << " maxrows=" << mx[w]
+               << " reduction=" << red[w] << " rows=[" << row[w] << "," << row[w] + riw[w] << ")\n";
+        }
+    }
+    return os.str();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ew_last_error(void) { return g_last_error.c_str(); }
+
+const char* ew_status_string(ew_status s) {
+    switch (s) {
+        case EW_OK: return "ok";
+        case EW_INVALID_ARGUMENT: return "invalid argument";
+        case EW_CG_DIVERGENCE: return "cg divergence";
+        case EW_UNSUPPORTED: return "unsupported";
+        case EW_CUDA: return "cuda error";
+        case EW_OUT_OF_MEMORY: return "out of memory";
+    }
+    return "unknown status";
+}
+
+int32_t ew_abi_version(void) { return EW_ABI_VERSION; }
+int32_t ew_kernel_id_count(void) { return kNumIds; }
+const char* ew_kernel_id(int32_t i) { return (i >= 0 && i < kNumIds) ? kIds[i] : nullptr; }
+int32_t ew_kernel_id_supported(const char* id) { return id ? id_support(id) : -1; }
+int64_t ew_launch_count(void) { return ew::g_launches.load(); }
+
+ew_status ew_csr_create(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets,
+                        int64_t nnz, const int64_t* col_indices, const double* values, ew_mem_kind mem,
+                        void* stream, ew_csr* out) {
+    return guarded([&] {
+        ew::require(out != nullptr, "out is null");
+        auto d = ew::csr_upload(nrows, ncols, n_row_offsets, row_offsets, nnz, col_indices, values, mem,
+                                ew::as_stream(stream));
+        *out = new ew_csr_t{std::move(d)};
+    });
+}
+
+ew_status ew_csr_destroy(ew_csr m) {
+    return guarded([&] { delete m; });
+}
+
+ew_status ew_csr_shape(ew_csr m, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        if (nrows) *nrows = m->d->nrows;
+        if (ncols) *ncols = m->d->ncols;
+        if (nnz) *nnz = m->d->nnz;
+    });
+}
+
+ew_status ew_csr_export(ew_csr m, int64_t* ro, int64_t* ci, double* v) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        const auto& d = *m->d;
+        if (ro) EW_CUDA_CHECK(cudaMemcpy(ro, d.ro.get(), (d.nrows + 1) * 8, cudaMemcpyDeviceToHost));
+        widen(d.ci, ci, d.nnz);
+        if (v && d.nnz) EW_CUDA_CHECK(cudaMemcpy(v, d.v.get(), d.nnz * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+ew_status ew_csr_update_values(ew_csr m, const double* v, ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        const auto& d = *m->d;
+        if (!d.nnz) return;
+        const auto kind = mem == EW_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        EW_CUDA_CHECK(cudaMemcpyAsync(d.v.get(), v, d.nnz * 8, kind, ew::as_stream(stream)));
+        if (mem == EW_MEM_HOST) EW_CUDA_CHECK(cudaStreamSynchronize(ew::as_stream(stream)));
+    });
+}
+
+ew_status ew_csr_spmv(ew_csr m, const double* x, int64_t nx, double* y, int64_t ny, ew_mem_kind mem,
+                      void* stream) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        const auto& d = *m->d;
+        ew::require(nx == d.ncols, "spmv dimension mismatch");
+        ew::require(ny == d.nrows, "spmv output length mismatch");
+        with_io(x, nx, y, ny, mem, ew::as_stream(stream),
+                [&](const double* xd, double* yd) { ew::csr_spmv(d, xd, yd, ew::as_stream(stream)); });
+    });
+}
+
+ew_status ew_csr_extract_diagonal(ew_csr m, double* diag, ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        const auto& d = *m->d;
+        with_io(nullptr, 0, diag, d.nrows, mem, ew::as_stream(stream),
+                [&](const double*, double* yd) { ew::csr_diagonal(d, yd, ew::as_stream(stream)); });
+    });
+}
+
+ew_status ew_sort_rows_desc(ew_csr m, int64_t* forward, int64_t* inverse) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        const auto& d = *m->d;
+        const int64_t n = d.nrows;
+        ew::DevBuf<int32_t> fwd(n), inv(n), slen(n);
+        ew::sort_rows_desc(d, fwd.get(), inv.get(), slen.get(), nullptr, nullptr);
+        EW_CUDA_CHECK(cudaDeviceSynchronize());
+        widen(fwd, forward, n);
+        widen(inv, inverse, n);
+    });
+}
+
+ew_status ew_reorder(ew_csr m, int32_t sort_within_rows, ew_csr* out, int64_t* forward) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        ew::require(out != nullptr, "out is null");
+        const int64_t n = m->d->nrows;
+        std::vector<int32_t> f(forward ? n : 0);
+        auto d = ew::reorder(*m->d, sort_within_rows != 0, forward ? f.data() : nullptr, nullptr);
+        if (forward)
+            for (int64_t i = 0; i < n; ++i) forward[i] = f[i];
+        *out = new ew_csr_t{std::move(d)};
+    });
+}
+
+ew_status ew_compute_k2_lanes(int64_t nnz_row, int64_t threshold, int64_t warp_size, int64_t* lanes) {
+    return guarded([&] {
+        ew::require(lanes != nullptr, "out is null");
+        *lanes = ew::compute_k2_lanes(nnz_row, threshold, warp_size);
+    });
+}
+
+ew_status ew_layout_build(ew_csr m, int32_t kind, const ew_warp_config* cfg, int64_t threshold,
+                          int32_t sort_rows, int32_t row_major, ew_layout* out) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        ew::require(out != nullptr, "out is null");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        auto d = ew::build_layout(*m->d, kind, c, threshold, sort_rows != 0, row_major != 0, nullptr);
+        *out = new ew_layout_t{std::move(d)};
+    });
+}
+
+ew_status ew_layout_import(const ew_layout_desc* desc, ew_layout* out) {
+    return guarded([&] {
+        ew::require(desc != nullptr && out != nullptr, "null argument");
+        *out = new ew_layout_t{ew::import_layout(*desc, nullptr)};
+    });
+}
+
+ew_status ew_layout_destroy(ew_layout l) {
+    return guarded([&] { delete l; });
+}
+
+ew_status ew_layout_get_info(ew_layout l, ew_layout_info* info) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        ew::require(info != nullptr, "info is null");
+        const auto& d = *l->d;
+        info->kind = d.kind;
+        info->warp_size = d.ws;
+        info->row_major = d.row_major;
+        info->sorted = d.sorted;
+        info->nrows = d.nrows;
+        info->ncols = d.ncols;
+        info->nnz = d.nnz;
+        info->nwarps = d.nwarps;
+        info->nslots = d.nslots;
+        info->stored_slots = d.stored_slots;
+        info->threshold = d.threshold;
+        info->device_bytes = static_cast<int64_t>(d.device_bytes());
+    });
+}
+
+ew_status ew_layout_export(ew_layout l, const ew_layout_arrays* out) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        ew::require(out != nullptr, "out is null");
+        const auto& d = *l->d;
+        if (out->values && d.nslots)
+            EW_CUDA_CHECK(cudaMemcpy(out->values, d.values.get(), d.nslots * 8, cudaMemcpyDeviceToHost));
+        widen(d.cols, out->col_indices, d.nslots);
+        if (out->warp_offset && d.nwarps)
+            EW_CUDA_CHECK(cudaMemcpy(out->warp_offset, d.warp_offset.get(), d.nwarps * 8,
+                                     cudaMemcpyDeviceToHost));
+        widen(d.maxrows, out->maxrows, d.nwarps);
+        widen(d.rows_in_warp, out->rows_in_warp, d.nwarps);
+        if (d.kind == EW_LAYOUT_K2) {
+            widen(d.reduction, out->reduction, d.nwarps);
+            widen(d.rows_offset_warp, out->rows_offset_warp, d.nwarps);
+        }
+        widen(d.fwd, out->forward, d.nrows);
+        widen(d.inv, out->inverse, d.nrows);
+        widen(d.slen, out->sorted_row_length, d.nrows);
+    });
+}
+
+ew_status ew_layout_value_slot_map(ew_layout l, ew_csr m, int64_t* map) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        check_handle(m, "csr");
+        ew::layout_build_slot_map(*l->d, *m->d, nullptr);
+        EW_CUDA_CHECK(cudaDeviceSynchronize());
+        if (map && m->d->nnz)
+            EW_CUDA_CHECK(cudaMemcpy(map, l->d->slot_map.get(), m->d->nnz * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+ew_status ew_layout_refresh_values(ew_layout l, ew_csr m, void* stream) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        check_handle(m, "csr");
+        ew::layout_refresh_values(*l->d, *m->d, ew::as_stream(stream));
+    });
+}
+
+ew_status ew_layout_dump(ew_layout l, char* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        const std::string s = dump(*l->d);
+        if (len) *len = s.size() + 1;
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, s.size());
+            std::memcpy(buf, s.data(), n);
+            buf[n] = '\0';
+        }
+    });
+}
+
+ew_status ew_layout_spmv(ew_layout l, const double* x, int64_t nx, double* y, int64_t ny, int32_t scatter,
+                         ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(l, "layout");
+        const auto& d = *l->d;
+        ew::require(nx == d.ncols, scatter ? "spmv_k1: dimension mismatch" : "spmv_k1: dimension mismatch");
+        ew::require(ny == d.nrows, "spmv output length mismatch");
+        with_io(x, nx, y, ny, mem, ew::as_stream(stream), [&](const double* xd, double* yd) {
+            ew::layout_spmv(d, xd, yd, scatter != 0, ew::as_stream(stream));
+        });
+    });
+}
+
+ew_status ew_kernel_prepare(const char* id, ew_csr m, const ew_warp_config* cfg,
+                            const ew_kernel_options* opts, ew_kernel* out) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        ew::require(out != nullptr && id != nullptr, "null argument");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        ew::validate_config(c);  // prepare_kernel validates first (kernels.cpp:61)
+        const std::string sid(id);
+        const int sup = id_support(sid);
+        if (sup < 0) throw ew::Error(EW_INVALID_ARGUMENT, "unknown kernel id '" + sid + "'");
+        if (sup == 0)
+            throw ew::Error(EW_UNSUPPORTED, "kernel '" + sid + "' has no device implementation yet");
+        const auto& src = m->d;
+        auto k = std::make_shared<ew::KernelData>();
+        k->id = sid;
+        k->nrows = src->nrows;
+        k->ncols = src->ncols;
+        k->nnz = src->nnz;
+        k->stored_slots = src->nnz;
+        if (sid == "csr_ref") {
+            k->csr = src;
+        } else {
+            const bool is_k2 = sid[1] == '2';
+            const bool reordered = sid.size() > 2;
+            const int64_t thr = o.k2_threshold > 0 ? o.k2_threshold : std::max<int64_t>(1, src->maxrow);
+            std::shared_ptr<ew::CsrData> op = src;
+            if (reordered) {
+                ew::require(src->nrows == src->ncols, "kernel '" + sid + "' requires a square matrix");
+                op = ew::reorder(*src, sid.back() == 's' && sid.size() == 4, nullptr, nullptr);
+            }
+            k->reordered = reordered;
+            k->layout = ew::build_layout(*op, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false,
+                                         nullptr);
+            k->stored_slots = k->layout->stored_slots;
+        }
+        auto* h = new ew_kernel_t{std::move(k), ew_layout_t{}};
+        h->layout_view.d = h->d->layout;
+        *out = h;
+    });
+}
+
+ew_status ew_kernel_destroy(ew_kernel k) {
+    return guarded([&] { delete k; });
+}
+
+ew_status ew_kernel_get_info(ew_kernel k, ew_kernel_info* info) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        ew::require(info != nullptr, "info is null");
+        const auto& d = *k->d;
+        std::memset(info, 0, sizeof(*info));
+        std::strncpy(info->id, d.id.c_str(), sizeof(info->id) - 1);
+        info->nrows = d.nrows;
+        info->ncols = d.ncols;
+        info->nnz = d.nnz;
+        info->stored_slots = d.stored_slots;
+        info->nwarps = d.layout ? d.layout->nwarps : 0;
+        info->has_perm = d.reordered ? 1 : 0;
+        info->layout_kind = d.layout ? d.layout->kind : 0;
+        info->device_bytes =
+            static_cast<int64_t>(d.layout ? d.layout->device_bytes() : d.csr->device_bytes());
+    });
+}
+
+ew_status ew_kernel_get_perm(ew_kernel k, int64_t* forward, int64_t* inverse) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        ew::require(k->d->reordered, "kernel '" + k->d->id + "' has no permutation");
+        widen(k->d->layout->fwd, forward, k->d->nrows);
+        widen(k->d->layout->inv, inverse, k->d->nrows);
+    });
+}
+
+ew_status ew_kernel_get_layout(ew_kernel k, ew_layout* out) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        ew::require(out != nullptr, "out is null");
+        *out = k->d->layout ? &k->layout_view : nullptr;
+    });
+}
+
+static ew_status apply_impl(ew_kernel k, const double* x, int64_t nx, double* y, int64_t ny,
+                            ew_mem_kind mem, void* stream, bool permuted) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        const auto& d = *k->d;
+        if (permuted && !d.reordered)
+            throw ew::Error(EW_INVALID_ARGUMENT, "kernel '" + d.id + "' has no apply_permuted");
+        ew::require(nx == d.ncols, "spmv dimension mismatch");
+        ew::require(ny == d.nrows, "spmv output length mismatch");
+        with_io(x, nx, y, ny, mem, ew::as_stream(stream), [&](const double* xd, double* yd) {
+            ew::kernel_apply(d, xd, yd, permuted, ew::as_stream(stream));
+        });
+    });
+}
+
+ew_status ew_kernel_apply(ew_kernel k, const double* x, int64_t nx, double* y, int64_t ny, ew_mem_kind mem,
+                          void* stream) {
+    return apply_impl(k, x, nx, y, ny, mem, stream, false);
+}
+
+ew_status ew_kernel_apply_permuted(ew_kernel k, const double* x, int64_t nx, double* y, int64_t ny,
+                                   ew_mem_kind mem, void* stream) {
+    return apply_impl(k, x, nx, y, ny, mem, stream, true);
+}
+
+ew_status ew_kernel_refresh_values(ew_kernel k, ew_csr m, void* stream) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        check_handle(m, "csr");
+        auto& d = *k->d;
+        const cudaStream_t s = ew::as_stream(stream);
+        ew::require(m->d->nrows == d.nrows && m->d->nnz == d.nnz, "refresh: structure mismatch");
+        if (d.csr) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(d.csr->v.get(), m->d->v.get(), d.nnz * 8, cudaMemcpyDeviceToDevice, s));
+            return;
+        }
+        if (d.reordered)
+            throw ew::Error(EW_UNSUPPORTED, "values-only refresh of r/rs kernels is not implemented yet");
+        ew::layout_refresh_values(*d.layout, *m->d, s);
+    });
+}
+
+static ew_status cg_impl(ew_kernel k, const double* b, const double* diag, int64_t n, const ew_cg_config* cfg,
+                         ew_mem_kind mem, double* x, double* history, ew_cg_result* result, void* stream,
+                         bool permuted) {
+    return guarded([&] {
+        check_handle(k, "kernel");
+        ew::require(cfg != nullptr && result != nullptr && b != nullptr && x != nullptr, "null argument");
+        const auto& d = *k->d;
+        if (permuted && !d.reordered)
+            throw ew::Error(EW_INVALID_ARGUMENT, "kernel '" + d.id + "' has no apply_permuted");
+        ew::require(n == d.nrows, "cg: b length does not match the operator");
+        const cudaStream_t s = ew::as_stream(stream);
+        const bool jac = cfg->jacobi != 0;
+        ew::require(!jac || diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+        ew::Scratch<double> bd(n, s), dd(jac ? n : 0, s), xd(n, s);
+        const auto kind = mem == EW_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        ew::Scratch<double> stage(permuted ? n : 0, s);
+        // cg_solve_permuted (cg.cpp:106-119): b and diag permuted once on entry
+        auto load = [&](const double* src, double* dst) {
+            if (!permuted) {
+                EW_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * 8, kind, s));
+            } else {
+                EW_CUDA_CHECK(cudaMemcpyAsync(stage.get(), src, n * 8, kind, s));
+                ew::gather(d.layout->fwd.get(), stage.get(), dst, n, s);
+            }
+        };
+        if (n) {
+            load(b, bd.get());
+            if (jac) load(diag, dd.get());
+        }
+        ew::KernelOperator op(d, permuted);
+        ew::CgOutputs o = ew::cg_device(op, bd.get(), jac ? dd.get() : nullptr, n, *cfg, xd.get(), s);
+        double* xsrc = xd.get();
+        if (permuted && n) {  // solution unpermuted once on exit
+            ew::scatter(d.layout->fwd.get(), xd.get(), stage.get(), n, s);
+            xsrc = stage.get();
+        }
+        if (n)
+            EW_CUDA_CHECK(cudaMemcpyAsync(x, xsrc, n * 8,
+                                          mem == EW_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                          s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        *result = o.res;
+        if (history)
+            std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+    });
+}
+
+ew_status ew_cg_solve(ew_kernel k, const double* b, const double* diag, int64_t n, const ew_cg_config* cfg,
+                      ew_mem_kind mem, double* x, double* history, ew_cg_result* result, void* stream) {
+    return cg_impl(k, b, diag, n, cfg, mem, x, history, result, stream, false);
+}
+
+ew_status ew_cg_solve_permuted(ew_kernel k, const double* b, const double* diag, int64_t n,
+                               const ew_cg_config* cfg, ew_mem_kind mem, double* x, double* history,
+                               ew_cg_result* result, void* stream) {
+    return cg_impl(k, b, diag, n, cfg, mem, x, history, result, stream, true);
+}
+
+namespace {
+struct CallbackOperator final : ew::CgOperator {
+    ew_operator_fn fn;
+    void* ctx;
+    int64_t n;
+    bool host_io;
+    double* hx;  // pinned staging for a host-memory callback
+    double* hy;
+    void apply(const double* x, double* y, cudaStream_t s, const int*) const override {
+        if (host_io && n) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(hx, x, n * 8, cudaMemcpyDeviceToHost, s));
+            EW_CUDA_CHECK(cudaStreamSynchronize(s));
+            const int rc = fn(ctx, hx, hy, s);
+            if (rc != 0) throw ew::Error(static_cast<ew_status>(rc), "cg: operator callback failed");
+            EW_CUDA_CHECK(cudaMemcpyAsync(y, hy, n * 8, cudaMemcpyHostToDevice, s));
+            return;
+        }
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        const int rc = fn(ctx, x, y, s);
+        if (rc != 0) throw ew::Error(static_cast<ew_status>(rc), "cg: operator callback failed");
+    }
+    bool host_callback() const override { return true; }
+    int64_t size() const override { return n; }
+};
+}  // namespace
+
+ew_status ew_cg_solve_operator(ew_operator_fn fn, void* ctx, ew_mem_kind op_mem, const double* b,
+                               const double* diag, int64_t n, const ew_cg_config* cfg, ew_mem_kind mem,
+                               double* x, double* history, ew_cg_result* result, void* stream) {
+    double* pinned = nullptr;
+    const ew_status st = guarded([&] {
+        ew::require(fn != nullptr && cfg != nullptr && result != nullptr && b != nullptr && x != nullptr,
+                    "null argument");
+        const cudaStream_t s = ew::as_stream(stream);
+        const bool jac = cfg->jacobi != 0;
+        ew::require(!jac || diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+        ew::Scratch<double> bd(n, s), dd(jac ? n : 0, s), xd(n, s);
+        const auto kind = mem == EW_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        if (n) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(bd.get(), b, n * 8, kind, s));
+            if (jac) EW_CUDA_CHECK(cudaMemcpyAsync(dd.get(), diag, n * 8, kind, s));
+        }
+        CallbackOperator op;
+        op.fn = fn;
+        op.ctx = ctx;
+        op.n = n;
+        op.host_io = op_mem == EW_MEM_HOST;
+        op.hx = op.hy = nullptr;
+        if (op.host_io && n) {
+            EW_CUDA_CHECK(cudaMallocHost(&pinned, 2 * n * sizeof(double)));
+            op.hx = pinned;
+            op.hy = pinned + n;
+        }
+        ew::CgOutputs o = ew::cg_device(op, bd.get(), jac ? dd.get() : nullptr, n, *cfg, xd.get(), s);
+        if (n)
+            EW_CUDA_CHECK(cudaMemcpyAsync(x, xd.get(), n * 8,
+                                          mem == EW_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                          s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        *result = o.res;
+        if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+    });
+    if (pinned) cudaFreeHost(pinned);
+    return st;
+}
+
+ew_status ew_compute_alpha(double t_reorder, double t_kernel, double t_base, int64_t* alpha, int32_t* finite) {
+    return guarded([&] {
+        // compute_alpha (cg.cpp:121-132); host arithmetic on four scalars
+        ew::require(t_reorder >= 0.0 && t_kernel >= 0.0 && t_base >= 0.0, "compute_alpha: negative time");
+        ew::require(alpha != nullptr && finite != nullptr, "null argument");
+        *alpha = -1;
+        *finite = 0;
+        if (t_kernel >= t_base) return;
+        const double ratio = t_reorder / (t_base - t_kernel);
+        *alpha = std::max<int64_t>(1, static_cast<int64_t>(std::ceil(ratio)));
+        *finite = 1;
+    });
+}
+
+}  // extern "C"

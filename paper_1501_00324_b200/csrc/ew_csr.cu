@@ -1,0 +1,162 @@
+// Device CSR: upload + validate_csr, the csr_ref SpMV, extract_diagonal,
+// permutation gather/scatter.
+#include "ew_internal.cuh"
+
+namespace ew {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+
+enum : int { kBadOrder = 1, kBadColumn = 2, kNotIncreasing = 4 };
+
+// validate_csr (csr.cpp:57-73) for one row per thread, plus int64 -> int32
+// column narrowing and the max row length. Flags OR into *err.
+__global__ void validate_rows_kernel(const int64_t* __restrict__ ro, const int64_t* __restrict__ ci64,
+                                     int32_t* __restrict__ ci32, int64_t nrows, int64_t ncols,
+                                     int64_t nnz, int* err, int* maxrow) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const int64_t lo = ro[r], hi = ro[r + 1];
+    if (lo > hi || lo < 0 || hi > nnz) {
+        atomicOr(err, kBadOrder);
+        return;
+    }
+    int64_t prev = -1;
+    int f = 0;
+    for (int64_t k = lo; k < hi; ++k) {
+        const int64_t c = ci64[k];
+        if (c < 0 || c >= ncols) f |= kBadColumn;
+        if (k > lo && prev >= c) f |= kNotIncreasing;
+        prev = c;
+        ci32[k] = static_cast<int32_t>(c);
+    }
+    if (f) atomicOr(err, f);
+    const int64_t len = hi - lo;
+    atomicMax(maxrow, static_cast<int>(len > 0x7fffffff ? 0x7fffffff : len));
+}
+
+// spmv_csr_reference (csr.cpp:75-86): one thread per row, sequential sum
+// from 0.0 in CSR order; mul and add rounded separately (no FMA), so the
+// result is bit-identical to the reference.
+__global__ void csr_scalar_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ v, const double* __restrict__ x,
+                                  double* __restrict__ y, int64_t nrows, const int* done) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows || (done && *done)) return;
+    double sum = 0.0;
+    for (int64_t k = ro[r], e = ro[r + 1]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], x[ci[k]]));
+    y[r] = sum;
+}
+
+// extract_diagonal (csr.cpp:106-117)
+__global__ void diagonal_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, double* __restrict__ d,
+                                int64_t nrows, int64_t ncols) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    double out = 0.0;
+    if (r < ncols) {
+        for (int64_t k = ro[r], e = ro[r + 1]; k < e; ++k) {
+            if (ci[k] == r) {
+                out = v[k];
+                break;
+            }
+        }
+    }
+    d[r] = out;
+}
+
+__global__ void gather_kernel(const int32_t* __restrict__ idx, const double* __restrict__ in,
+                              double* __restrict__ out, int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[idx[k]];
+}
+
+__global__ void scatter_kernel(const int32_t* __restrict__ idx, const double* __restrict__ in,
+                               double* __restrict__ out, int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[idx[k]] = in[k];
+}
+
+}  // namespace
+
+std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, const int64_t* ro,
+                                    int64_t nnz, const int64_t* ci, const double* v,
+                                    ew_mem_kind mem, cudaStream_t s) {
+    require(nrows >= 0 && ncols >= 0, "negative dimensions");
+    require(n_ro == nrows + 1, "row_offsets length");
+    require(nnz >= 0, "values/col_indices length mismatch");
+    if (nrows > 0x7fffffff || ncols > 0x7fffffff)
+        throw Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows and columns");
+    require(ro != nullptr, "row_offsets is null");
+    require(nnz == 0 || (ci != nullptr && v != nullptr), "col_indices/values are null");
+    auto m = std::make_shared<CsrData>();
+    m->nrows = nrows;
+    m->ncols = ncols;
+    m->nnz = nnz;
+    m->ro.alloc(nrows + 1);
+    m->ci.alloc(nnz);
+    m->v.alloc(nnz);
+    const auto kind = mem == EW_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    EW_CUDA_CHECK(cudaMemcpyAsync(m->ro.get(), ro, (nrows + 1) * sizeof(int64_t), kind, s));
+    if (nnz) EW_CUDA_CHECK(cudaMemcpyAsync(m->v.get(), v, nnz * sizeof(double), kind, s));
+    int64_t ends[2] = {0, 0};
+    EW_CUDA_CHECK(cudaMemcpyAsync(&ends[0], m->ro.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaMemcpyAsync(&ends[1], m->ro.get() + nrows, sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    require(ends[0] == 0, "row_offsets[0] != 0");
+    require(ends[1] == nnz, "row_offsets[nrows] != nnz");
+
+    Scratch<int64_t> ci64(nnz, s);
+    if (nnz) EW_CUDA_CHECK(cudaMemcpyAsync(ci64.get(), ci, nnz * sizeof(int64_t), kind, s));
+    Scratch<int> flags(2, s);
+    EW_CUDA_CHECK(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int), s));
+    if (nrows) {
+        validate_rows_kernel<<<grid_for(nrows), kBlock, 0, s>>>(m->ro.get(), ci64.get(), m->ci.get(),
+                                                                nrows, ncols, nnz, flags.get(),
+                                                                flags.get() + 1);
+        launched("validate_rows_kernel");
+    }
+    int h[2];
+    EW_CUDA_CHECK(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    require(!(h[0] & kBadOrder), "row_offsets not nondecreasing");
+    require(!(h[0] & kBadColumn), "column out of range");
+    require(!(h[0] & kNotIncreasing), "columns not strictly increasing within row");
+    m->maxrow = h[1];
+    return m;
+}
+
+void csr_spmv_guarded(const CsrData& m, const double* x, double* y, cudaStream_t s, const int* done) {
+    if (m.nrows == 0) return;
+    csr_scalar_kernel<<<grid_for(m.nrows), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), x, y,
+                                                           m.nrows, done);
+    launched("csr_scalar_kernel");
+}
+
+void csr_spmv(const CsrData& m, const double* x, double* y, cudaStream_t s) {
+    csr_spmv_guarded(m, x, y, s, nullptr);
+}
+
+void csr_diagonal(const CsrData& m, double* d, cudaStream_t s) {
+    if (m.nrows == 0) return;
+    diagonal_kernel<<<grid_for(m.nrows), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), d,
+                                                         m.nrows, m.ncols);
+    launched("diagonal_kernel");
+}
+
+void gather(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    gather_kernel<<<grid_for(n), kBlock, 0, s>>>(idx, in, out, n);
+    launched("gather_kernel");
+}
+
+void scatter(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    scatter_kernel<<<grid_for(n), kBlock, 0, s>>>(idx, in, out, n);
+    launched("scatter_kernel");
+}
+
+}  // namespace ew

@@ -1,0 +1,217 @@
+// Internal types shared by the CUDA translation units of libellwarp_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ellwarp_b200.h"
+
+namespace ew {
+
+// Raised inside the library, converted to an ew_status at the C boundary.
+struct Error : std::runtime_error {
+    ew_status status;
+    Error(ew_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void require(bool cond, const std::string& msg) {
+    if (!cond) throw Error(EW_INVALID_ARGUMENT, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        const ew_status s = (e == cudaErrorMemoryAllocation) ? EW_OUT_OF_MEMORY : EW_CUDA;
+        throw Error(s, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define EW_CUDA_CHECK(expr) ::ew::cuda_check((expr), #expr)
+
+// Launch accounting (the bench's gpu_launches claim and the smoke checks).
+extern std::atomic<int64_t> g_launches;
+inline void launched(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cuda_check(cudaGetLastError(), what);
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Owning device allocation (cudaMalloc; long-lived data: matrices, layouts).
+template <typename T>
+class DevBuf {
+  public:
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_, n_ = o.n_;
+            o.p_ = nullptr, o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(size_t n) {
+        release();
+        n_ = n;
+        if (n) EW_CUDA_CHECK(cudaMalloc(&p_, n * sizeof(T)));
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    size_t bytes() const { return n_ * sizeof(T); }
+
+  private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Stream-ordered scratch (cudaMallocAsync from the device's default pool).
+template <typename T>
+class Scratch {
+  public:
+    Scratch(size_t n, cudaStream_t s) : s_(s), n_(n) {
+        if (n) EW_CUDA_CHECK(cudaMallocAsync(&p_, n * sizeof(T), s));
+    }
+    ~Scratch() {
+        if (p_) cudaFreeAsync(p_, s_);
+    }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+
+  private:
+    T* p_ = nullptr;
+    cudaStream_t s_;
+    size_t n_;
+};
+
+// Device-resident CSR: int64 row offsets, int32 columns, fp64 values.
+struct CsrData {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int32_t maxrow = 0;
+    DevBuf<int64_t> ro;
+    DevBuf<int32_t> ci;
+    DevBuf<double> v;
+    size_t device_bytes() const { return ro.bytes() + ci.bytes() + v.bytes(); }
+};
+
+// Device ELL-WARP layout (K1 or K2). Per-warp metadata is int32 except the
+// int64 slot offsets; columns and permutations are int32.
+struct LayoutData {
+    int kind = EW_LAYOUT_K1;
+    int ws = 32;
+    int ws_log2 = 5;
+    int row_major = 0;
+    int sorted = 1;  // rows sorted longest-first: active rows are a prefix
+    int segment_bytes = 128;
+    int align = 1;
+    int64_t nrows = 0, ncols = 0, nnz = 0, nwarps = 0, nslots = 0, threshold = 0;
+    int64_t n_active = 0;  // rows with at least one entry
+    int64_t stored_slots = 0;
+    int32_t max_reduction = 1;
+    bool imported = false;  // built elsewhere: K2 may not cover every row
+    DevBuf<double> values;
+    DevBuf<int32_t> cols;
+    DevBuf<int64_t> warp_offset;
+    DevBuf<int32_t> maxrows, rows_in_warp, reduction, rows_offset_warp;
+    DevBuf<int32_t> fwd, inv, slen;
+    DevBuf<int64_t> slot_map;  // lazily built value_slot_map (values-only refresh)
+    size_t device_bytes() const {
+        return values.bytes() + cols.bytes() + warp_offset.bytes() + maxrows.bytes() +
+               rows_in_warp.bytes() + reduction.bytes() + rows_offset_warp.bytes() + fwd.bytes() +
+               inv.bytes() + slen.bytes() + slot_map.bytes();
+    }
+};
+
+struct KernelData {
+    std::string id;
+    int64_t nrows = 0, ncols = 0, nnz = 0, stored_slots = 0;
+    bool reordered = false;  // r / rs variants: perm set, apply permutes in/out
+    std::shared_ptr<CsrData> csr;        // csr_ref
+    std::shared_ptr<LayoutData> layout;  // k1* / k2*
+};
+
+// ---- internal API across translation units ---------------------------------
+void validate_config(const ew_warp_config& c);
+std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, const int64_t* ro,
+                                    int64_t nnz, const int64_t* ci, const double* v,
+                                    ew_mem_kind mem, cudaStream_t s);
+void csr_spmv(const CsrData& m, const double* x, double* y, cudaStream_t s);
+void csr_diagonal(const CsrData& m, double* d, cudaStream_t s);
+void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
+                    cudaStream_t s, unsigned long long* n_active_counter);
+std::shared_ptr<CsrData> reorder(const CsrData& m, bool sort_within_rows, int32_t* fwd_out,
+                                 cudaStream_t s);
+std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
+                                         int64_t threshold, bool sort_rows, bool row_major,
+                                         cudaStream_t s);
+std::shared_ptr<LayoutData> import_layout(const ew_layout_desc& d, cudaStream_t s);
+// done (nullable, device): the launch is a no-op once *done != 0 (CG overrun).
+void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
+                 const int* done = nullptr);
+void layout_build_slot_map(LayoutData& l, const CsrData& m, cudaStream_t s);
+void layout_refresh_values(LayoutData& l, const CsrData& m, cudaStream_t s);
+int64_t compute_k2_lanes(int64_t nnz_row, int64_t threshold, int64_t warp_size);
+void gather(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s);
+void scatter(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s);
+
+// Kernel-level operator: y = A x in the kernel's "apply" (original) or
+// "apply_permuted" (sorted) numbering; device pointers.
+void kernel_apply(const KernelData& k, const double* x, double* y, bool permuted,
+                  cudaStream_t s, const int* done = nullptr);
+void csr_spmv_guarded(const CsrData& m, const double* x, double* y, cudaStream_t s, const int* done);
+
+struct CgOutputs {
+    ew_cg_result res{};
+    std::vector<double> history;
+    ew_status status = EW_OK;
+    std::string message;
+};
+// The CG operator: y = A x on device pointers, enqueued on s. A host-callback
+// operator (the reference's arbitrary SpmvFn closure) runs synchronously on
+// the host thread; the solver then checks its done flag before each call.
+struct CgOperator {
+    virtual ~CgOperator() = default;
+    virtual void apply(const double* x, double* y, cudaStream_t s, const int* done) const = 0;
+    virtual bool host_callback() const { return false; }
+    virtual int64_t size() const = 0;
+};
+struct KernelOperator final : CgOperator {
+    const KernelData& k;
+    bool permuted;
+    KernelOperator(const KernelData& kd, bool p) : k(kd), permuted(p) {}
+    void apply(const double* x, double* y, cudaStream_t s, const int* done) const override {
+        kernel_apply(k, x, y, permuted, s, done);
+    }
+    int64_t size() const override { return k.nrows == k.ncols ? k.nrows : -1; }
+};
+// Device CG. b, diag, x are device pointers in the operator's numbering.
+CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, int64_t n,
+                    const ew_cg_config& cfg, double* x, cudaStream_t s);
+
+constexpr int kBlock = 256;
+inline unsigned grid_for(int64_t n, int block = kBlock) {
+    const int64_t g = (n + block - 1) / block;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+inline int log2_exact(int64_t v) {
+    int l = 0;
+    while ((int64_t{1} << l) < v) ++l;
+    return l;
+}
+
+}  // namespace ew

@@ -1,0 +1,258 @@
+// ELL-WARP SpMV kernels for sm_100a (paper Listings 1 and 2, PAPER.md:339-362,
+// 464-511; reference emulation warp_spmv.cpp:9-126).
+//
+// HBM-bound by design (0.16 flop/byte): each layout warp streams its own
+// contiguous slab of values (8 B) and int32 columns (4 B), column-major so
+// the 32 lanes of a step read 256 B + 128 B contiguous. The matrix stream is
+// loaded with L1::no_allocate + an L2 evict_first policy so the gathered x
+// vector keeps its L2 residency; x is read through the read-only path.
+//
+// Arithmetic is bit-identical to the reference: each lane sums
+// values[s]*x[col[s]] from 0.0 over all maxrows steps of its warp (padding
+// included), with the multiply and the add rounded separately (no FMA), and
+// K2 combines lane partials with the reference's ascending-stride pairwise
+// tree (stride 1, 2, 4, ...), done here with __shfl_down_sync.
+#include "ew_internal.cuh"
+
+namespace ew {
+
+namespace {
+
+struct StreamPolicy {
+    uint64_t p;
+};
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ double ld_x(const double* x, int32_t c) { return __ldg(x + c); }
+
+__device__ __forceinline__ double madd(double acc, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(a, b));  // two roundings, as the reference
+}
+
+struct K1Args {
+    const double* values;
+    const int32_t* cols;
+    const int64_t* woff;
+    const int32_t* maxrows;
+    const int32_t* slen;  // !SORTED only
+    const int32_t* fwd;   // SCATTER only
+    const double* x;
+    double* y;
+    const int* done;
+    int64_t nrows, n_active;
+    int32_t ws, ws_log2;
+};
+
+// Serial lane sum over j in [0, mx) at stride `step` from slot s, unrolled by
+// 8 so eight value/column loads and then eight x gathers are in flight per
+// thread before the (order-preserving) accumulation chain consumes them.
+__device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
+                                           const int32_t* __restrict__ cols,
+                                           const double* __restrict__ x, int64_t s, int64_t step,
+                                           int32_t mx, uint64_t pol) {
+    double sum = 0.0;
+    int32_t j = 0;
+    for (; j + 8 <= mx; j += 8) {
+        int32_t c[8];
+        double v[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = ld_stream(cols + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = ld_x(x, c[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum = madd(sum, v[u], xv[u]);
+        s += 8 * step;
+    }
+    if (j + 4 <= mx) {
+        int32_t c[4];
+        double v[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = ld_stream(cols + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = ld_x(x, c[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sum = madd(sum, v[u], xv[u]);
+        s += 4 * step;
+        j += 4;
+    }
+    for (; j < mx; ++j) {
+        sum = madd(sum, ld_stream(vals + s, pol), ld_x(x, ld_stream(cols + s, pol)));
+        s += step;
+    }
+    return sum;
+}
+
+// K1 / K1r / K1rs (warp_spmv.cpp:9-60): one thread per sorted row position.
+// SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
+template <bool SORTED, bool SCATTER, bool ROW_MAJOR>
+__global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= a.nrows || (a.done && *a.done)) return;
+    const uint64_t pol = evict_first_policy();
+    double sum = 0.0;
+    const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
+    if (active) {
+        const int64_t w = p >> a.ws_log2;
+        const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
+        const int32_t mx = a.maxrows[w];
+        const int64_t s = a.woff[w] + (ROW_MAJOR ? int64_t(lane) * mx : lane);
+        sum = lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
+    }
+    a.y[SCATTER ? a.fwd[p] : p] = sum;
+}
+
+struct K2Args {
+    const double* values;
+    const int32_t* cols;
+    const int64_t* woff;
+    const int32_t* maxrows;
+    const int32_t* reduction;
+    const int32_t* rows_offset_warp;
+    const int32_t* rows_in_warp;
+    const int32_t* slen;
+    const int32_t* fwd;
+    const double* x;
+    double* y;
+    const int* done;
+    int64_t nwarps, n_active;
+    int32_t ws, ws_log2;
+};
+
+// K2 / K2r / K2rs (warp_spmv.cpp:62-126) for warp_size <= 32: thread t is lane
+// t % ws of layout warp t / ws; `reduction` lanes share a row, each summing a
+// contiguous chunk of maxrows slots, then the ascending-stride tree.
+template <bool SORTED, bool SCATTER>
+__global__ void __launch_bounds__(256) k2_kernel(K2Args a) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w = t >> a.ws_log2;
+    const int32_t lane = static_cast<int32_t>(t & (a.ws - 1));
+    if (a.done && *a.done) return;  // uniform across the grid
+    const uint64_t pol = evict_first_policy();
+    double sum = 0.0;
+    int32_t red = 1, tl = 0;
+    bool leader = false;
+    int64_t pos = 0;
+    if (w < a.nwarps) {
+        red = a.reduction[w];
+        const int32_t rl = __ffs(red) - 1;
+        const int32_t r = lane >> rl;
+        tl = lane & (red - 1);
+        if (r < a.rows_in_warp[w]) {
+            pos = int64_t(a.rows_offset_warp[w]) + r;
+            leader = tl == 0;
+            const bool active = SORTED ? pos < a.n_active : a.slen[pos] > 0;
+            if (active) sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+        }
+    }
+    const int32_t hw_red = static_cast<int32_t>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(red)));
+    for (int32_t st = 1; st < hw_red; st <<= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, sum, st);
+        if (st < red && (tl & (2 * st - 1)) == 0) sum = __dadd_rn(sum, o);
+    }
+    if (leader) a.y[SCATTER ? a.fwd[pos] : pos] = sum;
+}
+
+// K2 for warp_size in (32, 1024]: one CTA of ws threads per layout warp, the
+// same tree through shared memory (the paper's sumvalues[] scratch).
+template <bool SORTED, bool SCATTER>
+__global__ void k2_wide_kernel(K2Args a) {
+    extern __shared__ double part[];
+    const int64_t w = blockIdx.x;
+    const int32_t lane = threadIdx.x;
+    if (a.done && *a.done) return;
+    const uint64_t pol = evict_first_policy();
+    const int32_t red = a.reduction[w];
+    const int32_t r = lane / red, tl = lane & (red - 1);
+    double sum = 0.0;
+    int64_t pos = 0;
+    const bool valid = r < a.rows_in_warp[w];
+    if (valid) {
+        pos = int64_t(a.rows_offset_warp[w]) + r;
+        const bool active = SORTED ? pos < a.n_active : a.slen[pos] > 0;
+        if (active) sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+    }
+    part[lane] = sum;
+    for (int32_t st = 1; st < red; st <<= 1) {
+        __syncthreads();
+        if ((tl & (2 * st - 1)) == 0) part[lane] = __dadd_rn(part[lane], part[lane + st]);
+    }
+    __syncthreads();
+    if (valid && tl == 0) a.y[SCATTER ? a.fwd[pos] : pos] = part[lane];
+}
+
+template <bool SORTED, bool SCATTER>
+void launch_k1(const K1Args& a, bool row_major, cudaStream_t s) {
+    if (row_major)
+        k1_kernel<SORTED, SCATTER, true><<<grid_for(a.nrows), kBlock, 0, s>>>(a);
+    else
+        k1_kernel<SORTED, SCATTER, false><<<grid_for(a.nrows), kBlock, 0, s>>>(a);
+    launched("k1_kernel");
+}
+
+template <bool SORTED, bool SCATTER>
+void launch_k2(const K2Args& a, cudaStream_t s) {
+    if (a.nwarps == 0) return;
+    if (a.ws <= 32) {
+        k2_kernel<SORTED, SCATTER><<<grid_for(a.nwarps * a.ws), kBlock, 0, s>>>(a);
+    } else {
+        k2_wide_kernel<SORTED, SCATTER><<<static_cast<unsigned>(a.nwarps), a.ws, a.ws * sizeof(double), s>>>(a);
+    }
+    launched("k2_kernel");
+}
+
+}  // namespace
+
+void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
+                 const int* done) {
+    if (l.nrows == 0) return;
+    if (l.kind == EW_LAYOUT_K1) {
+        K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
+                 l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
+        const bool rm = l.row_major != 0;
+        if (l.sorted) {
+            scatter ? launch_k1<true, true>(a, rm, s) : launch_k1<true, false>(a, rm, s);
+        } else {
+            scatter ? launch_k1<false, true>(a, rm, s) : launch_k1<false, false>(a, rm, s);
+        }
+        return;
+    }
+    // K2: packing covers every sorted position, so each y entry is written by
+    // exactly one leader; an imported layout may not, so y is cleared first
+    // (the reference starts from y = 0.0, warp_spmv.cpp:65).
+    if (l.imported) EW_CUDA_CHECK(cudaMemsetAsync(y, 0, l.nrows * sizeof(double), s));
+    K2Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.reduction.get(),
+             l.rows_offset_warp.get(), l.rows_in_warp.get(), l.slen.get(), l.fwd.get(), x, y, done,
+             l.nwarps, l.n_active, l.ws, l.ws_log2};
+    if (l.sorted) {
+        scatter ? launch_k2<true, true>(a, s) : launch_k2<true, false>(a, s);
+    } else {
+        scatter ? launch_k2<false, true>(a, s) : launch_k2<false, false>(a, s);
+    }
+}
+
+}  // namespace ew

@@ -1,0 +1,230 @@
+"""Synthetic FEM matrices of the shapes BASELINE.json names (host-side input
+synthesis only; the SpMV / CG under test never runs here).
+
+All meshes are the reference's structured tetrahedral box
+(fem/mesh.cpp:33-71): (nx+1)(ny+1)(nz+1) nodes numbered
+(k*(ny+1)+j)*(nx+1)+i, each cell split into six tetrahedra around its main
+diagonal (Freudenthal). P1 elements couple every node with itself and the
+14 neighbours at offsets +-x, +-y, +-z, +-(x+y), +-(y+z), +-(x+z),
++-(x+y+z): a 15-point stencil, 5..15 entries per row on the box.
+
+* ``laplacian_box``   -- config 1: P1 stiffness (element_geometry gradients,
+  fem/element.cpp:7-47) + sigma * lumped mass; SPD. box(63,63,63) gives
+  262,144 rows and 3,834,622 nonzeros.
+* ``elasticity_box``  -- config 2: 3-DOF linear elasticity (E, nu), 3x3
+  blocks on the same stencil + sigma * lumped mass; SPD.
+* ``ventricle_box``   -- config 4: config-1 operator on a mesh whose nodes
+  are jittered (per-element geometry) and whose unknowns are renumbered by a
+  seeded random permutation.
+
+Every generator returns (nrows, ncols, row_offsets[int64], col_indices[int64],
+values[float64]) with strictly increasing columns per row (canonical CSR).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# Freudenthal split (fem/mesh.cpp:52-71): corner walks of the six tetrahedra
+_PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+
+
+def _tet_corners():
+    """Per tetrahedron, its 4 corner offsets (di, dj, dk) in the cell."""
+    tets = []
+    for perm in _PERMS:
+        at = [0, 0, 0]
+        corners = [tuple(at)]
+        for s in range(3):
+            at[perm[s]] += 1
+            corners.append(tuple(at))
+        tets.append(corners)
+    return tets
+
+
+_STENCIL = sorted({(a[0] - b[0], a[1] - b[1], a[2] - b[2])
+                   for t in _tet_corners() for a in t for b in t})
+assert len(_STENCIL) == 15
+
+
+def _p1_gradients(xyz):
+    """P1 shape-function gradients and volumes for tets given as (..., 4, 3)
+    coordinates (element_geometry, fem/element.cpp:7-47)."""
+    e = xyz[..., 1:, :] - xyz[..., :1, :]  # rows: edge vectors from node 0
+    det = np.linalg.det(e)
+    inv = np.linalg.inv(e)  # columns: d xi / d x ... grad N_{1..3} are columns of inv^T rows
+    g123 = np.swapaxes(inv, -1, -2)  # (..., 3 nodes, 3 coords)
+    g0 = -g123.sum(axis=-2, keepdims=True)
+    grads = np.concatenate([g0, g123], axis=-2)
+    return grads, np.abs(det) / 6.0
+
+
+def _stencil_csr(nx, ny, nz, block, accumulate):
+    """CSR over the 15-point stencil with `block` x `block` node couplings.
+    accumulate(dense) fills dense[node, stencil_dir, a, b]."""
+    n1, n2, n3 = nx + 1, ny + 1, nz + 1
+    nn = n1 * n2 * n3
+    dense = np.zeros((nn, len(_STENCIL), block, block), np.float64)
+    accumulate(dense)
+    ii, jj, kk = np.meshgrid(np.arange(n1), np.arange(n2), np.arange(n3), indexing="ij")
+    ii, jj, kk = (a.transpose(2, 1, 0).ravel() for a in (ii, jj, kk))  # node order k, j, i
+    present = np.zeros((nn, len(_STENCIL)), bool)
+    offs = np.zeros(len(_STENCIL), np.int64)
+    for d, (di, dj, dk) in enumerate(_STENCIL):
+        present[:, d] = ((ii + di >= 0) & (ii + di < n1) & (jj + dj >= 0) & (jj + dj < n2)
+                         & (kk + dk >= 0) & (kk + dk < n3))
+        offs[d] = (dk * n2 + dj) * n1 + di
+    order = np.argsort(offs, kind="stable")  # ascending column within a node row
+    present, offs, dense = present[:, order], offs[order], dense[:, order]
+    node = np.arange(nn, dtype=np.int64)
+    # rows are (node, a); columns (node + off) * block + b, ascending per row
+    cnt_node = present.sum(axis=1) * block
+    row_len = np.repeat(cnt_node, block)
+    ro = np.zeros(nn * block + 1, np.int64)
+    np.cumsum(row_len, out=ro[1:])
+    cols = ((node[:, None] + offs[None, :])[:, :, None] * block + np.arange(block)[None, None, :])
+    cols = np.broadcast_to(cols[:, None, :, :], (nn, block, len(_STENCIL), block))
+    vals = np.transpose(dense, (0, 2, 1, 3))  # (node, a, dir, b)
+    mask = np.broadcast_to(present[:, None, :, None], (nn, block, len(_STENCIL), block))
+    ci = cols[mask].astype(np.int64)
+    v = vals[mask].astype(np.float64)
+    return nn * block, nn * block, ro, ci, v
+
+
+def _cells(nx, ny, nz):
+    ci, cj, ck = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    return (a.transpose(2, 1, 0).ravel() for a in (ci, cj, ck))
+
+
+def _node_id(i, j, k, nx, ny):
+    return (k * (ny + 1) + j) * (nx + 1) + i
+
+
+def _dir_index(d):
+    return _STENCIL.index(d)
+
+
+def laplacian_box(nx=63, ny=63, nz=63, sigma=1e-3):
+    """Config 1: P1 Laplacian stiffness + sigma * lumped mass, unit cells."""
+    tets = _tet_corners()
+
+    def acc(dense):
+        ci, cj, ck = _cells(nx, ny, nz)
+        base = _node_id(ci, cj, ck, nx, ny)
+        for corners in tets:
+            xyz = np.array(corners, np.float64)
+            g, vol = _p1_gradients(xyz)
+            ke = vol * g @ g.T
+            for a in range(4):
+                na = base + _node_id(*corners[a], nx, ny)
+                for b in range(4):
+                    d = _dir_index(tuple(np.subtract(corners[b], corners[a])))
+                    val = ke[a, b] + (sigma * vol / 4.0 if a == b else 0.0)
+                    # for a fixed corner every cell maps to a distinct node, so
+                    # a plain fancy-index add has no repeated indices
+                    dense[na, d, 0, 0] += val
+
+    return _stencil_csr(nx, ny, nz, 1, acc)
+
+
+def _elastic_d(E, nu):
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    D = np.zeros((6, 6))
+    D[:3, :3] = lam
+    D[np.arange(3), np.arange(3)] += 2 * mu
+    D[np.arange(3, 6), np.arange(3, 6)] = mu
+    return D
+
+
+def _strain_b(g):
+    """6 x 12 strain-displacement matrix of a P1 tet (Voigt xx,yy,zz,xy,yz,xz)."""
+    B = np.zeros((6, 12))
+    for a in range(4):
+        gx, gy, gz = g[a]
+        c = 3 * a
+        B[0, c] = gx
+        B[1, c + 1] = gy
+        B[2, c + 2] = gz
+        B[3, c], B[3, c + 1] = gy, gx
+        B[4, c + 1], B[4, c + 2] = gz, gy
+        B[5, c], B[5, c + 2] = gz, gx
+    return B
+
+
+def elasticity_box(nx=86, ny=86, nz=86, E=1.0, nu=0.3, sigma=1e-3):
+    """Config 2: 3-DOF linear elasticity + sigma * lumped mass (SPD)."""
+    tets = _tet_corners()
+    D = _elastic_d(E, nu)
+
+    def acc(dense):
+        ci, cj, ck = _cells(nx, ny, nz)
+        base = _node_id(ci, cj, ck, nx, ny)
+        for corners in tets:
+            xyz = np.array(corners, np.float64)
+            g, vol = _p1_gradients(xyz)
+            B = _strain_b(g)
+            ke = vol * B.T @ D @ B
+            for a in range(4):
+                na = base + _node_id(*corners[a], nx, ny)
+                for b in range(4):
+                    d = _dir_index(tuple(np.subtract(corners[b], corners[a])))
+                    blk = ke[3 * a:3 * a + 3, 3 * b:3 * b + 3].copy()
+                    if a == b:
+                        blk[np.arange(3), np.arange(3)] += sigma * vol / 4.0
+                    dense[na, d] += blk
+
+    return _stencil_csr(nx, ny, nz, 3, acc)
+
+
+def ventricle_box(nx=170, ny=170, nz=170, jitter=0.3, sigma=1e-3, seed=4, chunk_cells=2_000_000):
+    """Config 4: jittered P1 operator, unknowns renumbered at random."""
+    rng = np.random.default_rng(seed)
+    n1, n2, n3 = nx + 1, ny + 1, nz + 1
+    nn = n1 * n2 * n3
+    kk, jj, ii = np.meshgrid(np.arange(n3), np.arange(n2), np.arange(n1), indexing="ij")
+    xyz = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.float64)
+    xyz += rng.uniform(-jitter, jitter, size=xyz.shape)
+    tets = _tet_corners()
+
+    def acc(dense):
+        ci, cj, ck = _cells(nx, ny, nz)
+        base_all = _node_id(ci, cj, ck, nx, ny)
+        for lo in range(0, base_all.size, chunk_cells):
+            base = base_all[lo:lo + chunk_cells]
+            for corners in tets:
+                ids = np.stack([base + _node_id(*c, nx, ny) for c in corners], axis=1)
+                g, vol = _p1_gradients(xyz[ids])
+                ke = vol[:, None, None] * np.einsum("eaj,ebj->eab", g, g)
+                for a in range(4):
+                    for b in range(4):
+                        d = _dir_index(tuple(np.subtract(corners[b], corners[a])))
+                        val = ke[:, a, b] + (sigma * vol / 4.0 if a == b else 0.0)
+                        dense[ids[:, a], d, 0, 0] += val
+
+    n, _, ro, ci, v = _stencil_csr(nx, ny, nz, 1, acc)
+    perm = rng.permutation(n).astype(np.int64)  # new id of old unknown
+    return renumber(n, ro, ci, v, perm)
+
+
+def renumber(n, ro, ci, v, new_of_old):
+    """Symmetric renumbering P A P^T with columns re-sorted per row."""
+    rows_old = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+    r = new_of_old[rows_old]
+    c = new_of_old[ci]
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    ro2 = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=ro2[1:])
+    return n, n, ro2, c, v
+
+
+def random_x(n, seed=1):
+    """x = U(0.1, 1), the bench input (bench.cpp:27-33 draws it with
+    mt19937_64; any fixed seeded draw serves the throughput runs)."""
+    return np.random.default_rng(seed).uniform(0.1, 1.0, n)
+
+
+def stats(ro):
+    lens = np.diff(ro)
+    return dict(nrows=int(lens.size), nnz=int(ro[-1]), minrow=int(lens.min()), maxrow=int(lens.max()),
+                mean=float(lens.mean()))

@@ -1,0 +1,158 @@
+"""Device Jacobi PCG parity (cg.cpp:25-119) through the C ABI.
+
+Element-wise updates follow the reference bit for bit; the dot products use
+a fixed tree order instead of the reference's sequential sum, so residual
+histories are compared with the reference's own comparator
+|h_dev - h_ref| <= 1e-10 * (1 + h_ref) (test_solver.cpp:109-110,
+acceptance.cpp:377-378) over the same iteration count, and solutions within
+1e-10 relative (test_solver.cpp:79)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Csr
+from tests.gpu_helpers import rel_close
+
+pytestmark = pytest.mark.gpu
+
+HIST_TOL = 1e-10
+
+
+def _m(d):
+    return Csr.make(d["nrows"], d["ncols"], d["row_offsets"], d["col_indices"], d["values"])
+
+
+def dev_csr(ew, m):
+    return ew.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+
+
+def assert_history(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.size == want.size
+    assert np.all(np.abs(got - want) <= HIST_TOL * (1.0 + want)), np.max(np.abs(got - want) / (1 + want))
+
+
+def test_golden_histories(ew, R, golden):
+    for case in golden["cg"]:
+        m = _m(case["matrix"])
+        a = dev_csr(ew, m)
+        diag = a.extract_diagonal()
+        assert np.array_equal(diag, R.extract_diagonal(m))
+        for kid in ("csr_ref", "k1", "k1r", "k1rs", "k2", "k2r", "k2rs"):
+            k = ew.Kernel(kid, a)
+            res = k.cg_solve(case["b"], diag)
+            assert res.converged, kid
+            assert res.iterations == case["iterations"], (case["name"], kid)
+            assert res.spmv_calls == case["spmv_calls"]
+            assert_history(res.residual_history, case["history"])
+            assert rel_close(res.solution, case["solution"], 1e-10) or np.allclose(
+                res.solution, case["solution"], rtol=1e-10, atol=1e-12)
+            if k.has_perm:
+                rp = k.cg_solve(case["b"], diag, permuted=True)
+                assert rp.iterations == case["iterations"]
+                assert_history(rp.residual_history, case["history"])
+
+
+def test_laplacian_family_all_kernels(ew, R, F):
+    """acceptance.cpp criterion 6: identical iteration counts across kernels,
+    true residual <= 1e-8, permuted history within the comparator."""
+    for n in (4, 8, 12):
+        m = F.laplacian3d(n, n, n)
+        b = R.spmv_csr(m, np.ones(m.ncols))
+        ref = R.cg_csr(m, b)
+        a = dev_csr(ew, m)
+        diag = a.extract_diagonal()
+        for kid in ("csr_ref", "k1", "k1r", "k1rs", "k2", "k2r", "k2rs"):
+            res = ew.Kernel(kid, a).cg_solve(b, diag)
+            assert res.converged and res.iterations == ref.iterations, kid
+            ax = R.spmv_csr(m, res.solution)
+            assert np.sqrt(np.sum((b - ax) ** 2) / np.sum(b * b)) <= 1e-8
+            assert_history(res.residual_history, ref.residual_history)
+
+
+def test_identity_and_zero_rhs(ew, F):
+    eye = F.uniform_band(24, 1)
+    eye.values[:] = 1.0
+    b = F.random_vector(24, 3)
+    a = dev_csr(ew, eye)
+    res = ew.Kernel("k1", a).cg_solve(b, a.extract_diagonal())
+    assert res.converged and res.iterations == 1 and res.spmv_calls == 2  # test_solver.cpp:30-41
+    assert rel_close(res.solution, b, 1e-12)
+    res = ew.Kernel("k1", a).cg_solve(np.zeros(24), a.extract_diagonal())
+    assert res.converged and res.iterations == 0 and res.residual_history.tolist() == [0.0]
+
+
+def test_error_paths(ew, F):
+    m = F.laplacian3d(6, 6, 6)
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    res = k.cg_solve(F.random_vector(m.nrows, 17), a.extract_diagonal(), max_iterations=2)
+    assert not res.converged and res.iterations == 2
+    m2 = F.laplacian3d(2, 2, 2)
+    a2 = dev_csr(ew, m2)
+    b = np.ones(m2.nrows)
+    b[3] = np.nan
+    with pytest.raises(ew.CgDivergenceError):
+        ew.Kernel("csr_ref", a2).cg_solve(b, a2.extract_diagonal())
+    neg = F.uniform_band(8, 1)
+    neg.values[:] = -1.0
+    with pytest.raises(ew.CgDivergenceError):
+        ew.Kernel("k1", dev_csr(ew, neg)).cg_solve(np.ones(8), None, jacobi=False)
+    with pytest.raises(ValueError):
+        k.cg_solve(np.ones(m.nrows), None, jacobi=True)  # jacobi needs the diagonal
+    with pytest.raises(ValueError):
+        k.cg_solve(np.ones(m.nrows), a.extract_diagonal(), tol=0.0)
+    zd = a.extract_diagonal()
+    zd[5] = 0.0
+    with pytest.raises(ValueError):
+        k.cg_solve(np.ones(m.nrows), zd)
+    with pytest.raises(ValueError):
+        k.cg_solve(np.ones(m.nrows), a.extract_diagonal(), permuted=True)  # k1 has no perm
+
+
+def test_jacobi_never_hurts(ew, F):
+    """test_solver.cpp:145-160."""
+    for n in (2, 3, 4, 5):
+        m = F.laplacian3d(n, n, n)
+        b = F.random_vector(m.nrows, 100 + n)
+        a = dev_csr(ew, m)
+        k = ew.Kernel("k1rs", a)
+        rj = k.cg_solve(b, a.extract_diagonal())
+        rn = k.cg_solve(b, None, jacobi=False)
+        assert rj.converged and rn.converged and rj.iterations <= rn.iterations
+
+
+def test_no_jacobi_history(ew, R, F):
+    m = F.fem_tet_graph(600, 5, 21, 12)
+    b = F.random_vector(m.nrows, 31)
+    ref = R.cg_csr(m, b, jacobi=False)
+    res = ew.Kernel("k2", dev_csr(ew, m), threshold=4).cg_solve(b, None, jacobi=False)
+    assert res.iterations == ref.iterations
+    assert_history(res.residual_history, ref.residual_history)
+
+
+def test_operator_callback(ew, R, F):
+    """cg_solve with an arbitrary SpmvFn closure (cg.hpp:32-40)."""
+    m = F.laplacian3d(5, 5, 5)
+    b = R.spmv_csr(m, np.ones(m.ncols))
+    ref = R.cg_csr(m, b)
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    res = ew.cg_solve_operator(lambda v: k.apply(v), b, a.extract_diagonal())
+    assert res.iterations == ref.iterations and res.spmv_calls == ref.spmv_calls
+    assert_history(res.residual_history, ref.residual_history)
+
+
+def test_recompute_interval_and_long_run(ew, R, F):
+    """Forced-length runs (tol tiny): 1000 iterations, refresh every 50 --
+    the bench configuration -- stay within the comparator until stagnation."""
+    m = F.fem_tet_graph(2000, 5, 21, 3)
+    b = F.random_vector(m.nrows, 5)
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1rs", a)
+    for interval in (0, 7, 50):
+        ref = R.cg_csr(m, b, tol=1e-300, max_iterations=300, recompute=interval)
+        res = k.cg_solve(b, a.extract_diagonal(), tol=1e-300, max_iterations=300, recompute_interval=interval)
+        assert res.iterations == 300 and not res.converged
+        assert res.spmv_calls == ref.spmv_calls
+        assert_history(res.residual_history, ref.residual_history)

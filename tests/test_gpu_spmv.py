@@ -1,0 +1,176 @@
+"""SpMV parity on the device, through the C ABI, against the restated oracle
+and the reference's own criteria (test_ellwarp.cpp:276-386, acceptance.cpp
+criterion 2). The device kernels keep the reference's per-lane summation
+order, so every comparison except the csr-order oracle is bitwise."""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import bits, oracle_apply, rel_close, same
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = ["csr_ref", "k1", "k1r", "k1rs", "k2", "k2r", "k2rs"]
+
+
+def dev_csr(ew, m):
+    return ew.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+
+
+def test_worked_example(ew, R, golden):
+    from oracle.oracle import Csr
+
+    g = golden["worked"]
+    m = Csr.make(**{k: g["matrix"][k] for k in ("nrows", "ncols")}, ro=g["matrix"]["row_offsets"],
+                 ci=g["matrix"]["col_indices"], v=g["matrix"]["values"])
+    a = dev_csr(ew, m)
+    for kid in KERNELS:
+        y = ew.Kernel(kid, a).apply(g["x"])
+        assert y.tolist() == g["y"], kid
+    k = ew.Kernel("k1r", a)
+    fwd, inv = k.perm()
+    assert fwd.tolist() == g["forward"]
+    yp = k.apply_permuted(np.asarray(g["x"])[fwd])
+    assert yp[inv[0]] == 121.0
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_corpus_all_kernels(ew, R, F, case):
+    m = F.random_case(case)
+    x = F.random_vector(m.ncols, 5000 + case)
+    oracle = R.spmv_csr(m, x)
+    a = dev_csr(ew, m)
+    assert np.array_equal(bits(a.spmv(x)), bits(oracle))  # csr_ref on device: bit-identical
+    for ws in (4, 8, 32):
+        for kid in KERNELS:
+            if kid.endswith(("r", "rs")) and m.nrows != m.ncols:
+                with pytest.raises(ValueError):
+                    ew.Kernel(kid, a, warp_size=ws)
+                continue
+            y = ew.Kernel(kid, a, warp_size=ws).apply(x)
+            assert np.array_equal(bits(y), bits(oracle_apply(R, kid, m, x, ws))), (kid, ws)
+            assert rel_close(y, oracle, 1e-12), (kid, ws)
+        if kid in ("k1", "k2"):
+            pass
+
+
+@pytest.mark.parametrize("case", range(0, 40, 3))
+def test_corpus_k2_threshold_sweep(ew, R, F, case):
+    """acceptance.cpp:168-183: the full T sweep for the K2 family."""
+    m = F.random_case(case)
+    x = F.random_vector(m.ncols, 6000 + case)
+    oracle = R.spmv_csr(m, x)
+    a = dev_csr(ew, m)
+    lens = np.diff(m.row_offsets)
+    lo = max(1, int(lens.min()))
+    hi = max(lo, int(lens.max()))
+    for ws in (4, 32):
+        for t in range(lo, hi + 1, max(1, (hi - lo) // 12)):
+            for kid in ("k2", "k2r", "k2rs"):
+                if kid != "k2" and m.nrows != m.ncols:
+                    continue
+                y = ew.Kernel(kid, a, warp_size=ws, threshold=t).apply(x)
+                assert np.array_equal(bits(y), bits(oracle_apply(R, kid, m, x, ws, t))), (kid, ws, t)
+                assert rel_close(y, oracle, 1e-12)
+
+
+def test_apply_permuted(ew, R, F):
+    for case in range(0, 16):
+        m = F.random_case(case)
+        if m.nrows != m.ncols:
+            continue
+        x = F.random_vector(m.ncols, 77 + case)
+        a = dev_csr(ew, m)
+        for kid in ("k1r", "k1rs", "k2r", "k2rs"):
+            k = ew.Kernel(kid, a, threshold=3)
+            y = k.apply_permuted(x)
+            assert np.array_equal(bits(y), bits(oracle_apply(R, kid, m, x, 32, 3, permuted=True))), kid
+        for kid in ("csr_ref", "k1", "k2"):
+            with pytest.raises(ValueError):
+                ew.Kernel(kid, a).apply_permuted(x)
+
+
+def test_k2_equals_k1_at_maxrow(ew, F):
+    """acceptance.cpp:326-329: T >= maxrow is bitwise K1."""
+    for case in range(12):
+        m = F.random_case(case)
+        x = F.random_vector(m.ncols, 600 + case)
+        a = dev_csr(ew, m)
+        t = max(1, int(np.diff(m.row_offsets).max()))
+        y1 = ew.Kernel("k1", a).apply(x)
+        y2 = ew.Kernel("k2", a, threshold=t).apply(x)
+        assert np.array_equal(bits(y1), bits(y2))
+
+
+def test_four_lane_sum(ew, golden):
+    g = golden["four_lane"]["matrix"]
+    a = ew.Csr(g["nrows"], g["ncols"], g["row_offsets"], g["col_indices"], g["values"])
+    assert ew.Kernel("k2", a, threshold=2).apply(np.ones(8))[0] == 255.0
+
+
+def test_wide_and_row_major_layouts(ew, R, F):
+    """warp_size 64 (K2 through shared memory) and the row_major diagnostic."""
+    m = F.powerlaw_rows(300, 1.5, 120, 3)
+    x = F.random_vector(m.ncols, 17)
+    a = dev_csr(ew, m)
+    for t in (1, 3, 10, 40, 120):
+        y = ew.Kernel("k2", a, warp_size=64, threshold=t).apply(x)
+        assert np.array_equal(bits(y), bits(oracle_apply(R, "k2", m, x, 64, t)))
+    lay = ew.Layout.build(a, "k1", row_major=True)
+    lr = R.build_k1(m, row_major=True)
+    assert np.array_equal(lay.export().values, lr.values)
+    assert np.array_equal(bits(lay.spmv(x)), bits(R.spmv_layout(lr, x)))
+
+
+def test_errors(ew, F):
+    m = F.random_csr(5, 7, 0.5, 3)
+    a = dev_csr(ew, m)
+    with pytest.raises(ValueError):
+        ew.Kernel("k1r", a)  # kernels.cpp:25 non-square
+    with pytest.raises(ValueError):
+        ew.Kernel("nope", a)
+    with pytest.raises(ValueError):
+        ew.Kernel("k1", a, warp_size=12)  # warp_model.cpp:8
+    with pytest.raises(ew.UnsupportedError):
+        ew.Kernel("ell", a)
+    with pytest.raises(ValueError):
+        ew.Kernel("k1", a).apply(np.ones(6))  # dimension mismatch
+    with pytest.raises(ValueError):
+        ew.Csr(2, 2, [0, 1, 2], [1, 0], [1.0])  # length mismatch
+    with pytest.raises(ValueError):
+        ew.Csr(2, 2, [0, 2, 2], [1, 0], [1.0, 1.0])  # not increasing
+    with pytest.raises(ValueError):
+        ew.Csr(2, 2, [0, 1, 2], [0, 2], [1.0, 1.0])  # column out of range
+    with pytest.raises(ValueError):
+        ew.Csr(2, 2, [0, 1, 3], [0, 1], [1.0, 1.0])  # row_offsets[n] != nnz
+
+
+def test_empty_rows_and_empty_matrix(ew, R):
+    from oracle.oracle import Csr
+
+    # rows with no entries keep y = 0.0 (warp_spmv.cpp:21-24), incl. a NaN x[0]
+    m = Csr.make(6, 6, [0, 0, 2, 2, 3, 3, 3], [0, 4, 5], [1.0, 2.0, 3.0])
+    x = np.array([np.nan, 1, 2, 3, 4, 5], np.float64)
+    a = dev_csr(ew, m)
+    for kid in KERNELS:
+        y = ew.Kernel(kid, a, threshold=1).apply(x)
+        want = oracle_apply(R, kid, m, x, 32, 1)
+        assert same(y, want), kid
+    z = Csr.make(0, 0, [0], [], [])
+    az = dev_csr(ew, z)
+    assert ew.Kernel("k1", az).apply(np.zeros(0)).size == 0
+
+
+def test_device_buffers_and_streams(ew, R, F):
+    import torch
+
+    m = F.random_case(5)
+    x = F.random_vector(m.ncols, 3)
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    s = torch.cuda.Stream()
+    xd = torch.tensor(x, device="cuda")
+    yd = torch.empty(m.nrows, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        k.apply(xd, yd, stream=s)
+    s.synchronize()
+    assert np.array_equal(bits(yd.cpu().numpy()), bits(oracle_apply(R, "k1", m, x)))

@@ -1,0 +1,132 @@
+"""Pins the C restatement oracle (oracle/ew_oracle.c) before any device result
+is compared with it: against the reference tests' golden vectors
+(tests/golden/golden.json) and against the real reference compiled from its
+sources (oracle/_ref) on the reference's own randomized corpus
+(proj/tests/test_support.hpp:29-50). CPU only."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Csr
+
+
+def _m(d):
+    return Csr.make(d["nrows"], d["ncols"], d["row_offsets"], d["col_indices"], d["values"])
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.int64)
+
+
+def test_worked_example(R, golden):
+    g = golden["worked"]
+    m = _m(g["matrix"])
+    fwd, inv = R.sort_rows_desc(m)
+    assert fwd.tolist() == g["forward"] == [1, 4, 6, 2, 0, 3, 5]
+    r_op, _ = R.reorder(m, False)
+    rs_op, _ = R.reorder(m, True)
+    assert r_op.col_indices[:5].tolist() == g["c_prime"] == [4, 0, 5, 1, 6]
+    assert rs_op.col_indices[:5].tolist() == g["c_second"] == [0, 1, 4, 5, 6]
+    assert rs_op.values[:5].tolist() == g["a_second"] == [8.0, 10.0, 7.0, 9.0, 2.0]
+    y = R.spmv_csr(m, g["x"])
+    assert y[0] == 121.0 and y.tolist() == g["y"]
+    lay = R.build_k1(m)
+    assert R.spmv_layout(lay, g["x"]).tolist() == g["y"]
+    # K1r: sorted kernel on the r operand, unpermuted, bitwise equal to K1
+    lay_r = R.build_k1(r_op)
+    yp = R.spmv_layout(lay_r, np.asarray(g["x"])[fwd], scatter=False)
+    assert yp[inv[0]] == 121.0
+
+
+def test_small_goldens(R, golden):
+    assert R.sort_rows_desc(_m(golden["sort_132"]["matrix"]))[0].tolist() == [1, 2, 0]
+    g = golden["k1_four_rows"]
+    lay = R.build_k1(_m(g["matrix"]), warp_size=4)
+    assert lay.maxrows.tolist() == g["maxrows"] and lay.stored_slots == 16 and lay.padded_slots == 6
+    for nnz, t, ws, want in golden["k2_lanes"]:
+        assert R.compute_k2_lanes(nnz, t, ws) == want
+    g = golden["k2_100_8"]
+    lay = R.build_k2(_m(g["matrix"]), g["threshold"])
+    assert lay.reduction[0] == 16 and lay.rows_in_warp[0] == 1 and lay.maxrows[0] == 7
+    assert all(r == 1 for r in lay.reduction[1:])
+    g = golden["four_lane"]
+    lay = R.build_k2(_m(g["matrix"]), g["threshold"])
+    assert R.spmv_layout(lay, np.ones(8))[0] == 255.0
+
+
+def test_compute_alpha(R):
+    # test_solver.cpp:162-204
+    assert R.compute_alpha(10.0, 1.0, 2.0) == 10
+    assert R.compute_alpha(10.0, 2.0, 2.0) is None
+    assert R.compute_alpha(0.0, 3.0, 2.0) is None
+    assert R.compute_alpha(0.0, 1.0, 2.0) == 1
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_restatement_matches_reference_corpus(R, F, case):
+    m = F.random_case(case)
+    x = F.random_vector(m.ncols, 400 + case)
+    assert np.array_equal(bits(R.spmv_csr(m, x)), bits(F.spmv_csr(m, x)))
+    assert all(np.array_equal(a, b) for a, b in zip(R.sort_rows_desc(m), F.sort_rows_desc(m)))
+    for ws in (4, 8, 32):
+        lr = R.build_k1(m, warp_size=ws)
+        lf = F.build("k1", m, warp_size=ws)
+        for f in ("values", "col_indices", "warp_offset", "maxrows", "rows_in_warp", "forward",
+                  "sorted_row_length"):
+            assert np.array_equal(getattr(lr, f), getattr(lf, f)), f
+        assert lr.stored_slots == lf.stored_slots
+        assert np.array_equal(R.value_slot_map(lr, m), lf.value_slot_map)
+        assert np.array_equal(bits(R.spmv_layout(lr, x)), bits(F.apply("k1", m, x, warp_size=ws)))
+        R.free(lr)
+        mx = max(1, int(np.diff(m.row_offsets).max()))
+        for t in sorted({1, 2, 3, max(1, mx // 3), mx}):
+            lr = R.build_k2(m, t, warp_size=ws)
+            lf = F.build("k2", m, warp_size=ws, threshold=t)
+            for f in ("values", "col_indices", "warp_offset", "maxrows", "rows_in_warp", "reduction",
+                      "rows_offset_warp", "forward", "sorted_row_length"):
+                assert np.array_equal(getattr(lr, f), getattr(lf, f)), (f, t)
+            assert np.array_equal(R.value_slot_map(lr, m), lf.value_slot_map)
+            assert np.array_equal(bits(R.spmv_layout(lr, x)),
+                                  bits(F.apply("k2", m, x, warp_size=ws, threshold=t)))
+            R.free(lr)
+    if m.nrows == m.ncols:
+        for rs in (False, True):
+            a, fa = R.reorder(m, rs)
+            b, fb = F.reorder(m, rs)
+            assert np.array_equal(a.col_indices, b.col_indices) and np.array_equal(a.values, b.values)
+            assert np.array_equal(fa, fb)
+
+
+def test_restatement_cg_matches_reference(R, F, golden):
+    for case in golden["cg"]:
+        m = _m(case["matrix"])
+        if case["permuted"]:
+            op, _ = R.reorder(m, True)
+            lay = R.build_k1(op)
+            res = R.cg_layout(lay, case["b"], diag=R.extract_diagonal(m), permuted=True)
+        else:
+            res = R.cg_csr(m, case["b"])
+        assert res.iterations == case["iterations"]
+        assert res.spmv_calls == case["spmv_calls"]
+        # same operation order -> bitwise-identical history and solution
+        assert np.array_equal(bits(res.residual_history), bits(case["history"])), case["name"]
+        assert np.array_equal(bits(res.solution), bits(case["solution"])), case["name"]
+
+
+def test_restatement_cg_error_paths(R, F):
+    # test_solver.cpp:115-143
+    from oracle.oracle import OracleError
+
+    a = F.laplacian3d(6, 6, 6)
+    res = R.cg_csr(a, F.random_vector(a.nrows, 17), max_iterations=2)
+    assert not res.converged and res.iterations == 2
+    a = F.laplacian3d(2, 2, 2)
+    b = np.ones(a.nrows)
+    b[3] = np.nan
+    with pytest.raises(OracleError) as e:
+        R.cg_csr(a, b)
+    assert e.value.code == 2
+    eye = F.uniform_band(8, 1)
+    eye.values[:] = -1.0
+    with pytest.raises(OracleError) as e:
+        R.cg_csr(eye, np.ones(8), jacobi=False)
+    assert e.value.code == 2
