@@ -86,6 +86,10 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t = time.time()
+            while not self.rows and time.time() - t < 5.0:  # sampler live before timing starts
+                time.sleep(0.01)
+            self.rows.clear()
         except FileNotFoundError:
             self.proc = None
         return self

@@ -60,7 +60,7 @@ void with_io(const double* x, int64_t nx, double* y, int64_t ny, ew_mem_kind mem
              Op&& op) {
     if (mem == EW_MEM_DEVICE) {
         op(x, y);
-        ew::launched("with_io(device)");  // surfaces async launch errors
+        EW_CUDA_CHECK(cudaGetLastError());  // surfaces async launch errors
         return;
     }
     ew::Scratch<double> xd(nx, s), yd(ny, s);

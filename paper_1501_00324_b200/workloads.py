@@ -176,30 +176,46 @@ def elasticity_box(nx=86, ny=86, nz=86, E=1.0, nu=0.3, sigma=1e-3):
     return _stencil_csr(nx, ny, nz, 3, acc)
 
 
-def ventricle_box(nx=170, ny=170, nz=170, jitter=0.3, sigma=1e-3, seed=4, chunk_cells=2_000_000):
+def _tet_grad_vol(p0, p1, p2, p3):
+    """Closed-form P1 gradients (4 x (..., 3)) and volumes of tets whose corner
+    coordinates are (..., 3) arrays (element_geometry, fem/element.cpp:7-47)."""
+    e1, e2, e3 = p1 - p0, p2 - p0, p3 - p0
+    c23 = np.cross(e2, e3)
+    c31 = np.cross(e3, e1)
+    c12 = np.cross(e1, e2)
+    det = np.einsum("...j,...j->...", e1, c23)
+    g1 = c23 / det[..., None]
+    g2 = c31 / det[..., None]
+    g3 = c12 / det[..., None]
+    g0 = -(g1 + g2 + g3)
+    return (g0, g1, g2, g3), np.abs(det) / 6.0
+
+
+def ventricle_box(nx=170, ny=170, nz=170, jitter=0.3, sigma=1e-3, seed=4, slab=16):
     """Config 4: jittered P1 operator, unknowns renumbered at random."""
     rng = np.random.default_rng(seed)
     n1, n2, n3 = nx + 1, ny + 1, nz + 1
-    nn = n1 * n2 * n3
     kk, jj, ii = np.meshgrid(np.arange(n3), np.arange(n2), np.arange(n1), indexing="ij")
-    xyz = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.float64)
+    xyz = np.stack([ii, jj, kk], axis=-1).astype(np.float64)  # (n3, n2, n1, 3)
     xyz += rng.uniform(-jitter, jitter, size=xyz.shape)
     tets = _tet_corners()
 
     def acc(dense):
-        ci, cj, ck = _cells(nx, ny, nz)
-        base_all = _node_id(ci, cj, ck, nx, ny)
-        for lo in range(0, base_all.size, chunk_cells):
-            base = base_all[lo:lo + chunk_cells]
+        d3 = dense.reshape(n3, n2, n1, len(_STENCIL))
+        for k0 in range(0, nz, slab):
+            k1 = min(nz, k0 + slab)
             for corners in tets:
-                ids = np.stack([base + _node_id(*c, nx, ny) for c in corners], axis=1)
-                g, vol = _p1_gradients(xyz[ids])
-                ke = vol[:, None, None] * np.einsum("eaj,ebj->eab", g, g)
+                pts = [xyz[k0 + c[2]:k1 + c[2], c[1]:ny + c[1], c[0]:nx + c[0]] for c in corners]
+                grads, vol = _tet_grad_vol(*pts)
                 for a in range(4):
+                    ca = corners[a]
+                    tgt = d3[k0 + ca[2]:k1 + ca[2], ca[1]:ny + ca[1], ca[0]:nx + ca[0]]
                     for b in range(4):
                         d = _dir_index(tuple(np.subtract(corners[b], corners[a])))
-                        val = ke[:, a, b] + (sigma * vol / 4.0 if a == b else 0.0)
-                        dense[ids[:, a], d, 0, 0] += val
+                        val = vol * np.einsum("...j,...j->...", grads[a], grads[b])
+                        if a == b:
+                            val += sigma * vol / 4.0
+                        tgt[..., d] += val
 
     n, _, ro, ci, v = _stencil_csr(nx, ny, nz, 1, acc)
     perm = rng.permutation(n).astype(np.int64)  # new id of old unknown
@@ -208,14 +224,24 @@ def ventricle_box(nx=170, ny=170, nz=170, jitter=0.3, sigma=1e-3, seed=4, chunk_
 
 def renumber(n, ro, ci, v, new_of_old):
     """Symmetric renumbering P A P^T with columns re-sorted per row."""
-    rows_old = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
-    r = new_of_old[rows_old]
-    c = new_of_old[ci]
-    order = np.lexsort((c, r))
-    r, c, v = r[order], c[order], v[order]
+    lens = np.diff(ro)
+    width = int(lens.max()) if n else 0
+    old_of_new = np.empty(n, np.int64)
+    old_of_new[new_of_old] = np.arange(n, dtype=np.int64)
+    new_lens = lens[old_of_new]
     ro2 = np.zeros(n + 1, np.int64)
-    np.cumsum(np.bincount(r, minlength=n), out=ro2[1:])
-    return n, n, ro2, c, v
+    np.cumsum(new_lens, out=ro2[1:])
+    # rows padded to `width`, sorted by new column, padding sorts last
+    slot = np.arange(width)[None, :]
+    src = ro[old_of_new][:, None] + slot
+    valid = slot < new_lens[:, None]
+    src = np.where(valid, src, 0)
+    cols = np.where(valid, new_of_old[ci[src]], np.iinfo(np.int64).max)
+    order = np.argsort(cols, axis=1, kind="stable")
+    cols = np.take_along_axis(cols, order, axis=1)
+    vals = np.take_along_axis(v[src], order, axis=1)
+    keep = np.take_along_axis(valid, order, axis=1)
+    return n, n, ro2, cols[keep], vals[keep]
 
 
 def random_x(n, seed=1):
