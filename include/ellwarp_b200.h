@@ -163,10 +163,16 @@ int32_t ew_kernel_id_supported(const char* id);
 int64_t ew_launch_count(void);
 
 /* ---- matrices (csr.hpp / csr.cpp) --------------------------------------- */
-/* Upload + validate_csr (csr.cpp:57-73) on the device. */
+/* Upload + validate_csr (csr.cpp:57-73) on the device. Row offsets and
+ * column ranges are always checked (memory safety); the strictly-increasing
+ * column check runs with EW_CSR_CANONICAL. Without it the matrix may hold a
+ * renumbered r operand (reorder.hpp:17), which the reference feeds to
+ * build_k1 / build_k2 unsorted. */
+#define EW_CSR_CANONICAL 1
 ew_status ew_csr_create(int64_t nrows, int64_t ncols, int64_t n_row_offsets,
                         const int64_t* row_offsets, int64_t nnz, const int64_t* col_indices,
-                        const double* values, ew_mem_kind mem, void* stream, ew_csr* out);
+                        const double* values, ew_mem_kind mem, int32_t flags, void* stream,
+                        ew_csr* out);
 ew_status ew_csr_destroy(ew_csr m);
 ew_status ew_csr_shape(ew_csr m, int64_t* nrows, int64_t* ncols, int64_t* nnz);
 ew_status ew_csr_export(ew_csr m, int64_t* row_offsets, int64_t* col_indices, double* values);
@@ -182,8 +188,20 @@ ew_status ew_csr_extract_diagonal(ew_csr m, double* diag, ew_mem_kind mem, void*
 /* sort_rows_desc (permutation.cpp:49-55): stable, longest first. Host out. */
 ew_status ew_sort_rows_desc(ew_csr m, int64_t* forward, int64_t* inverse);
 /* make_reordered_r (reorder.cpp:8-17), + make_reordered_rs (:19-43) when
- * sort_within_rows; forward (host, nrows, nullable) receives the permutation. */
-ew_status ew_reorder(ew_csr m, int32_t sort_within_rows, ew_csr* out, int64_t* forward);
+ * sort_within_rows. forward_in (host, nrows) is the permutation to renumber
+ * by (Permutation::from_forward checks, permutation.cpp:17-28); NULL means
+ * sort_rows_desc(m), as prepare_kernel does (kernels.cpp:26). forward_out
+ * (host, nrows, nullable) receives the permutation used. */
+ew_status ew_reorder(ew_csr m, const int64_t* forward_in, int32_t sort_within_rows, ew_csr* out,
+                     int64_t* forward_out);
+/* The per-row (column, value) sort of make_reordered_rs on its own
+ * (reorder.cpp:26-41): columns ascending within every row. */
+ew_status ew_csr_sort_rows(ew_csr m, ew_csr* out);
+/* apply_forward (permutation.cpp:35-40): out[k] = in[forward[k]], or with
+ * inverse = 1 apply_inverse (:42-47): out[forward[k]] = in[k].
+ * forward is host int64[n]; in/out live in `mem`. */
+ew_status ew_permute(const int64_t* forward, int64_t n, const double* in, double* out,
+                     int32_t inverse, ew_mem_kind mem, void* stream);
 /* compute_k2_lanes (warp_layout.cpp:76-84) */
 ew_status ew_compute_k2_lanes(int64_t nnz_row, int64_t threshold, int64_t warp_size,
                               int64_t* lanes);

@@ -109,8 +109,8 @@ _SIGS = {
     "ew_kernel_id": (C.c_char_p, [C.c_int32]),
     "ew_kernel_id_supported": (C.c_int32, [C.c_char_p]),
     "ew_launch_count": (C.c_int64, []),
-    "ew_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_int, _vp,
-                                C.POINTER(_vp)]),
+    "ew_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_int, C.c_int32,
+                                _vp, C.POINTER(_vp)]),
     "ew_csr_destroy": (C.c_int, [_vp]),
     "ew_csr_shape": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
     "ew_csr_export": (C.c_int, [_vp, _vp, _vp, _vp]),
@@ -118,7 +118,9 @@ _SIGS = {
     "ew_csr_spmv": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int, _vp]),
     "ew_csr_extract_diagonal": (C.c_int, [_vp, _vp, C.c_int, _vp]),
     "ew_sort_rows_desc": (C.c_int, [_vp, _vp, _vp]),
-    "ew_reorder": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), _vp]),
+    "ew_reorder": (C.c_int, [_vp, _vp, C.c_int32, C.POINTER(_vp), _vp]),
+    "ew_csr_sort_rows": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ew_permute": (C.c_int, [_vp, C.c_int64, _vp, _vp, C.c_int32, C.c_int, _vp]),
     "ew_compute_k2_lanes": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _i64p]),
     "ew_layout_build": (C.c_int, [_vp, C.c_int32, C.POINTER(WarpConfig), C.c_int64, C.c_int32, C.c_int32,
                                   C.POINTER(_vp)]),
@@ -223,7 +225,7 @@ def _mem_of(a):
 class Csr:
     """Device-resident SparseCsr (ew_csr)."""
 
-    def __init__(self, nrows, ncols, row_offsets, col_indices, values, stream=None):
+    def __init__(self, nrows, ncols, row_offsets, col_indices, values, stream=None, canonical=True):
         ro = row_offsets if hasattr(row_offsets, "data_ptr") else _host(row_offsets, np.int64)
         ci = col_indices if hasattr(col_indices, "data_ptr") else _host(col_indices, np.int64)
         v = values if hasattr(values, "data_ptr") else _host(values, np.float64)
@@ -234,7 +236,7 @@ class Csr:
             raise ValueError("values/col_indices length mismatch")
         h = C.c_void_p()
         check(lib().ew_csr_create(int(nrows), int(ncols), int(nro), _ptr(ro), int(nnz), _ptr(ci), _ptr(v),
-                                  _mem_of(ro), _stream_ptr(stream), C.byref(h)))
+                                  _mem_of(ro), 1 if canonical else 0, _stream_ptr(stream), C.byref(h)))
         self.h = h
         self.nrows, self.ncols, self.nnz = int(nrows), int(ncols), int(nnz)
 
@@ -284,11 +286,29 @@ class Csr:
         check(lib().ew_sort_rows_desc(self.h, _ptr(fwd), _ptr(inv)))
         return fwd, inv
 
-    def reorder(self, sort_within_rows=False):
+    def reorder(self, sort_within_rows=False, forward=None):
+        """make_reordered_r (+ rs); forward=None renumbers by sort_rows_desc."""
         h = C.c_void_p()
         fwd = np.empty(self.nrows, np.int64)
-        check(lib().ew_reorder(self.h, 1 if sort_within_rows else 0, C.byref(h), _ptr(fwd)))
-        return Csr._wrap(h), fwd
+        fin = _host(forward, np.int64) if forward is not None else None
+        check(lib().ew_reorder(self.h, _ptr(fin), 1 if sort_within_rows else 0, C.byref(h), _ptr(fwd)))
+        return Csr._wrap(h), (fwd if forward is None else fin.copy())
+
+    def sort_rows(self):
+        h = C.c_void_p()
+        check(lib().ew_csr_sort_rows(self.h, C.byref(h)))
+        return Csr._wrap(h)
+
+
+def permute(forward, x, inverse=False):
+    """apply_forward / apply_inverse (permutation.cpp:35-47) on the device."""
+    f = _host(forward, np.int64)
+    xh = _host(x, np.float64)
+    if xh.size != f.size:
+        raise ValueError("permutation size mismatch")
+    out = np.empty(f.size, np.float64)
+    check(lib().ew_permute(_ptr(f), f.size, _ptr(xh), _ptr(out), 1 if inverse else 0, EW_MEM_HOST, None))
+    return out
 
 
 def _apply(fn, x, y, nx, ny, stream):

@@ -140,11 +140,11 @@ int64_t ew_launch_count(void) { return ew::g_launches.load(); }
 
 ew_status ew_csr_create(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets,
                         int64_t nnz, const int64_t* col_indices, const double* values, ew_mem_kind mem,
-                        void* stream, ew_csr* out) {
+                        int32_t flags, void* stream, ew_csr* out) {
     return guarded([&] {
         ew::require(out != nullptr, "out is null");
         auto d = ew::csr_upload(nrows, ncols, n_row_offsets, row_offsets, nnz, col_indices, values, mem,
-                                ew::as_stream(stream));
+                                (flags & EW_CSR_CANONICAL) != 0, ew::as_stream(stream));
         *out = new ew_csr_t{std::move(d)};
     });
 }
@@ -217,16 +217,48 @@ ew_status ew_sort_rows_desc(ew_csr m, int64_t* forward, int64_t* inverse) {
     });
 }
 
-ew_status ew_reorder(ew_csr m, int32_t sort_within_rows, ew_csr* out, int64_t* forward) {
+ew_status ew_reorder(ew_csr m, const int64_t* forward_in, int32_t sort_within_rows, ew_csr* out,
+                     int64_t* forward) {
     return guarded([&] {
         check_handle(m, "csr");
         ew::require(out != nullptr, "out is null");
         const int64_t n = m->d->nrows;
         std::vector<int32_t> f(forward ? n : 0);
-        auto d = ew::reorder(*m->d, sort_within_rows != 0, forward ? f.data() : nullptr, nullptr);
+        auto d = ew::reorder(*m->d, forward_in, true, sort_within_rows != 0, forward ? f.data() : nullptr,
+                             nullptr);
         if (forward)
             for (int64_t i = 0; i < n; ++i) forward[i] = f[i];
         *out = new ew_csr_t{std::move(d)};
+    });
+}
+
+ew_status ew_csr_sort_rows(ew_csr m, ew_csr* out) {
+    return guarded([&] {
+        check_handle(m, "csr");
+        ew::require(out != nullptr, "out is null");
+        *out = new ew_csr_t{ew::reorder(*m->d, nullptr, false, true, nullptr, nullptr)};
+    });
+}
+
+ew_status ew_permute(const int64_t* forward, int64_t n, const double* in, double* out, int32_t inverse,
+                     ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        ew::require(forward != nullptr || n == 0, "permutation is null");
+        const cudaStream_t s = ew::as_stream(stream);
+        std::vector<int32_t> hf(static_cast<size_t>(n));
+        for (int64_t k = 0; k < n; ++k) {
+            ew::require(forward[k] >= 0 && forward[k] < n, "permutation index out of range");
+            hf[k] = static_cast<int32_t>(forward[k]);
+        }
+        ew::Scratch<int32_t> fd(n, s);
+        if (n) EW_CUDA_CHECK(cudaMemcpyAsync(fd.get(), hf.data(), n * 4, cudaMemcpyHostToDevice, s));
+        with_io(in, n, out, n, mem, s, [&](const double* xd, double* yd) {
+            if (inverse)
+                ew::scatter(fd.get(), xd, yd, n, s);  // out[forward[k]] = in[k]
+            else
+                ew::gather(fd.get(), xd, yd, n, s);  // out[k] = in[forward[k]]
+        });
+        if (mem == EW_MEM_DEVICE) EW_CUDA_CHECK(cudaStreamSynchronize(s));  // host staging lifetime
     });
 }
 
@@ -376,7 +408,7 @@ ew_status ew_kernel_prepare(const char* id, ew_csr m, const ew_warp_config* cfg,
             std::shared_ptr<ew::CsrData> op = src;
             if (reordered) {
                 ew::require(src->nrows == src->ncols, "kernel '" + sid + "' requires a square matrix");
-                op = ew::reorder(*src, sid.back() == 's' && sid.size() == 4, nullptr, nullptr);
+                op = ew::reorder(*src, nullptr, true, sid.back() == 's' && sid.size() == 4, nullptr, nullptr);
             }
             k->reordered = reordered;
             k->layout = ew::build_layout(*op, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false,

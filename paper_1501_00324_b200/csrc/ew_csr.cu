@@ -83,7 +83,7 @@ __global__ void scatter_kernel(const int32_t* __restrict__ idx, const double* __
 
 std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, const int64_t* ro,
                                     int64_t nnz, const int64_t* ci, const double* v,
-                                    ew_mem_kind mem, cudaStream_t s) {
+                                    ew_mem_kind mem, bool canonical, cudaStream_t s) {
     require(nrows >= 0 && ncols >= 0, "negative dimensions");
     require(n_ro == nrows + 1, "row_offsets length");
     require(nnz >= 0, "values/col_indices length mismatch");
@@ -124,7 +124,7 @@ std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, 
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     require(!(h[0] & kBadOrder), "row_offsets not nondecreasing");
     require(!(h[0] & kBadColumn), "column out of range");
-    require(!(h[0] & kNotIncreasing), "columns not strictly increasing within row");
+    require(!canonical || !(h[0] & kNotIncreasing), "columns not strictly increasing within row");
     m->maxrow = h[1];
     return m;
 }

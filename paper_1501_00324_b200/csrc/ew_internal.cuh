@@ -149,13 +149,16 @@ struct KernelData {
 void validate_config(const ew_warp_config& c);
 std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, const int64_t* ro,
                                     int64_t nnz, const int64_t* ci, const double* v,
-                                    ew_mem_kind mem, cudaStream_t s);
+                                    ew_mem_kind mem, bool canonical, cudaStream_t s);
 void csr_spmv(const CsrData& m, const double* x, double* y, cudaStream_t s);
 void csr_diagonal(const CsrData& m, double* d, cudaStream_t s);
 void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
                     cudaStream_t s, unsigned long long* n_active_counter);
-std::shared_ptr<CsrData> reorder(const CsrData& m, bool sort_within_rows, int32_t* fwd_out,
-                                 cudaStream_t s);
+// make_reordered_r / make_reordered_rs (reorder.cpp:8-43): renumber columns
+// by a permutation (fwd_in, host, nullable = sort_rows_desc) and/or sort each
+// row's (column, value) pairs by column.
+std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool renumber,
+                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s);
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s);

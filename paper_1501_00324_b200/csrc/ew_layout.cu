@@ -235,7 +235,8 @@ __global__ void row_rank_sort_kernel(const int64_t* __restrict__ ro, const int32
         for (int64_t k = lo + lane; k < hi; k += 32) {
             const int32_t c = c_in[k];
             int64_t rank = 0;
-            for (int64_t q = lo; q < hi; ++q) rank += c_in[q] < c ? 1 : 0;
+            // stable rank; keys are distinct for a renumbered canonical row
+            for (int64_t q = lo; q < hi; ++q) rank += (c_in[q] < c || (c_in[q] == c && q < k)) ? 1 : 0;
             c_out[lo + rank] = c;
             v_out[lo + rank] = v_in[k];
         }
@@ -329,14 +330,34 @@ void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
     launched("finish_perm_kernel");
 }
 
-std::shared_ptr<CsrData> reorder(const CsrData& m, bool sort_within_rows, int32_t* fwd_out,
-                                 cudaStream_t s) {
-    require(m.nrows == m.ncols, "make_reordered_r: matrix must be square");
+std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool renumber,
+                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s) {
     const int64_t n = m.nrows, nnz = m.nnz;
-    Scratch<int32_t> fwd(n, s), inv(n, s), slen(n, s);
-    sort_rows_desc(m, fwd.get(), inv.get(), slen.get(), s, nullptr);
+    Scratch<int32_t> fwd(renumber ? n : 0, s), inv(renumber ? n : 0, s), slen(renumber ? n : 0, s);
+    if (renumber) {
+        require(m.nrows == m.ncols, "make_reordered_r: matrix must be square");
+        if (fwd_in) {
+            // Permutation::from_forward (permutation.cpp:17-28) semantics
+            std::vector<int32_t> hf(static_cast<size_t>(n)), hi(static_cast<size_t>(n), -1);
+            for (int64_t k = 0; k < n; ++k) {
+                const int64_t old = fwd_in[k];
+                require(old >= 0 && old < n, "permutation index out of range");
+                require(hi[old] == -1, "permutation not a bijection");
+                hi[old] = static_cast<int32_t>(k);
+                hf[k] = static_cast<int32_t>(old);
+            }
+            if (n) {
+                EW_CUDA_CHECK(cudaMemcpyAsync(fwd.get(), hf.data(), n * 4, cudaMemcpyHostToDevice, s));
+                EW_CUDA_CHECK(cudaMemcpyAsync(inv.get(), hi.data(), n * 4, cudaMemcpyHostToDevice, s));
+                EW_CUDA_CHECK(cudaStreamSynchronize(s));  // host staging goes out of scope
+            }
+        } else {
+            sort_rows_desc(m, fwd.get(), inv.get(), slen.get(), s, nullptr);
+        }
+    }
     auto out = std::make_shared<CsrData>();
-    out->nrows = out->ncols = n;
+    out->nrows = n;
+    out->ncols = m.ncols;
     out->nnz = nnz;
     out->maxrow = m.maxrow;
     out->ro.alloc(n + 1);
@@ -345,21 +366,24 @@ std::shared_ptr<CsrData> reorder(const CsrData& m, bool sort_within_rows, int32_
     EW_CUDA_CHECK(cudaMemcpyAsync(out->ro.get(), m.ro.get(), (n + 1) * sizeof(int64_t),
                                   cudaMemcpyDeviceToDevice, s));
     if (nnz) {
-        if (!sort_within_rows) {
-            renumber_kernel<<<grid_for(nnz), kBlock, 0, s>>>(m.ci.get(), inv.get(), out->ci.get(), nnz);
+        Scratch<int32_t> tmp(sort_within_rows ? nnz : 0, s);
+        int32_t* cdst = sort_within_rows ? tmp.get() : out->ci.get();
+        if (renumber) {
+            renumber_kernel<<<grid_for(nnz), kBlock, 0, s>>>(m.ci.get(), inv.get(), cdst, nnz);
             launched("renumber_kernel");
+        } else {
+            EW_CUDA_CHECK(cudaMemcpyAsync(cdst, m.ci.get(), nnz * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        if (sort_within_rows) {
+            row_rank_sort_kernel<<<fill_grid(n), 256, 0, s>>>(m.ro.get(), tmp.get(), m.v.get(),
+                                                              out->ci.get(), out->v.get(), n);
+            launched("row_rank_sort_kernel");
+        } else {
             EW_CUDA_CHECK(cudaMemcpyAsync(out->v.get(), m.v.get(), nnz * sizeof(double),
                                           cudaMemcpyDeviceToDevice, s));
-        } else {
-            Scratch<int32_t> tmp(nnz, s);
-            renumber_kernel<<<grid_for(nnz), kBlock, 0, s>>>(m.ci.get(), inv.get(), tmp.get(), nnz);
-            launched("renumber_kernel");
-            row_rank_sort_kernel<<<fill_grid((n + 0)), 256, 0, s>>>(m.ro.get(), tmp.get(), m.v.get(),
-                                                                   out->ci.get(), out->v.get(), n);
-            launched("row_rank_sort_kernel");
         }
     }
-    if (fwd_out && n)
+    if (fwd_out && renumber && n)
         EW_CUDA_CHECK(cudaMemcpyAsync(fwd_out, fwd.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     return out;
