@@ -44,10 +44,7 @@ constexpr int kNumIds = 11;
 
 int id_support(const std::string& id) {
     for (int i = 0; i < kNumIds; ++i) {
-        if (id == kIds[i]) {
-            if (id == "csr_vector" || id == "coo" || id == "ell" || id == "hyb") return 0;
-            return 1;
-        }
+        if (id == kIds[i]) return 1;  // every reference kernel id runs on the device
     }
     return -1;
 }
@@ -400,7 +397,12 @@ ew_status ew_kernel_prepare(const char* id, ew_csr m, const ew_warp_config* cfg,
         k->nnz = src->nnz;
         k->stored_slots = src->nnz;
         if (sid == "csr_ref") {
-            k->csr = src;
+            k->csr = ew::csr_clone(*src, nullptr);
+        } else if (sid == "csr_vector" || sid == "coo" || sid == "ell" || sid == "hyb") {
+            if (c.warp_size > 1024) throw ew::Error(EW_UNSUPPORTED, "warp_size above 1024 has no device mapping");
+            k->csr = ew::csr_clone(*src, nullptr);
+            k->format = ew::build_format(*src, sid, c.warp_size, o.hyb_k_ell, nullptr);
+            k->stored_slots = k->format->stored_slots;
         } else {
             const bool is_k2 = sid[1] == '2';
             const bool reordered = sid.size() > 2;
@@ -439,8 +441,9 @@ ew_status ew_kernel_get_info(ew_kernel k, ew_kernel_info* info) {
         info->nwarps = d.layout ? d.layout->nwarps : 0;
         info->has_perm = d.reordered ? 1 : 0;
         info->layout_kind = d.layout ? d.layout->kind : 0;
-        info->device_bytes =
-            static_cast<int64_t>(d.layout ? d.layout->device_bytes() : d.csr->device_bytes());
+        info->device_bytes = static_cast<int64_t>(
+            d.layout ? d.layout->device_bytes()
+                     : d.csr->device_bytes() + (d.format ? d.format->device_bytes() : size_t{0}));
     });
 }
 
@@ -493,6 +496,8 @@ ew_status ew_kernel_refresh_values(ew_kernel k, ew_csr m, void* stream) {
         auto& d = *k->d;
         const cudaStream_t s = ew::as_stream(stream);
         ew::require(m->d->nrows == d.nrows && m->d->nnz == d.nnz, "refresh: structure mismatch");
+        if (d.format && (d.format->kind == ew::FormatData::kEll || d.format->kind == ew::FormatData::kHyb))
+            throw ew::Error(EW_UNSUPPORTED, "values-only refresh of ell/hyb kernels is not implemented");
         if (d.csr) {
             EW_CUDA_CHECK(cudaMemcpyAsync(d.csr->v.get(), m->d->v.get(), d.nnz * 8, cudaMemcpyDeviceToDevice, s));
             return;

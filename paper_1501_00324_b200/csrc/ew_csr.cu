@@ -129,6 +129,26 @@ std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, 
     return m;
 }
 
+std::shared_ptr<CsrData> csr_clone(const CsrData& m, cudaStream_t s) {
+    // prepared kernels own their matrix, as the reference's closures own a
+    // copy (kernels.cpp:65-68): later updates of the caller's handle do not
+    // reach an already prepared kernel
+    auto c = std::make_shared<CsrData>();
+    c->nrows = m.nrows;
+    c->ncols = m.ncols;
+    c->nnz = m.nnz;
+    c->maxrow = m.maxrow;
+    c->ro.alloc(m.nrows + 1);
+    c->ci.alloc(m.nnz);
+    c->v.alloc(m.nnz);
+    EW_CUDA_CHECK(cudaMemcpyAsync(c->ro.get(), m.ro.get(), c->ro.bytes(), cudaMemcpyDeviceToDevice, s));
+    if (m.nnz) {
+        EW_CUDA_CHECK(cudaMemcpyAsync(c->ci.get(), m.ci.get(), c->ci.bytes(), cudaMemcpyDeviceToDevice, s));
+        EW_CUDA_CHECK(cudaMemcpyAsync(c->v.get(), m.v.get(), c->v.bytes(), cudaMemcpyDeviceToDevice, s));
+    }
+    return c;
+}
+
 void csr_spmv_guarded(const CsrData& m, const double* x, double* y, cudaStream_t s, const int* done) {
     if (m.nrows == 0) return;
     csr_scalar_kernel<<<grid_for(m.nrows), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), x, y,

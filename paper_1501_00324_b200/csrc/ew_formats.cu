@@ -1,0 +1,336 @@
+// The paper's comparison formats on the device: ELL,
+// HYB, COO segmented scan and CSR-vector, with the reference emulation's
+// exact arithmetic order (formats.cpp:7-235) so that every kernel id of
+// prepare_kernel runs on the B200 and matches the reference bit for bit.
+//
+// These are baselines, not the product's hot path: they are written to be
+// correct and coalesced, not tuned. Virtual warps of `ws` lanes live in
+// CTAs of max(256, ws) threads; reductions and scans go through shared
+// memory with the reference's ascending strides.
+#include "ew_internal.cuh"
+
+namespace ew {
+
+namespace {
+
+__device__ __forceinline__ double madd(double acc, double a, double b) { return __dadd_rn(acc, __dmul_rn(a, b)); }
+
+// ELL / HYB ELL part (formats.cpp:7-52): element (r, j) at j * nrows + r,
+// padding value 0.0 at column 0; each row keeps its first `width` entries.
+__global__ void ell_build_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ v, int64_t n, int64_t width,
+                                 double* __restrict__ ev, int32_t* __restrict__ ec) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t lo = ro[r], len = ro[r + 1] - lo;
+    for (int64_t j = 0; j < width; ++j) {
+        const bool real_entry = j < len;
+        ev[j * n + r] = real_entry ? v[lo + j] : 0.0;
+        ec[j * n + r] = real_entry ? ci[lo + j] : 0;
+    }
+}
+
+// spmv_ell (formats.cpp:64-95): y[r] = 0.0, then every slot incl. padding.
+__global__ void ell_spmv_kernel(const double* __restrict__ ev, const int32_t* __restrict__ ec, int64_t n,
+                                int64_t width, const double* __restrict__ x, double* __restrict__ y,
+                                const int* done) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n || (done && *done)) return;
+    double s = 0.0;
+    for (int64_t j = 0; j < width; ++j) s = madd(s, ev[j * n + r], __ldg(x + ec[j * n + r]));
+    y[r] = s;
+}
+
+// spmv_csr_vector (formats.cpp:194-235): a virtual warp of ws lanes per
+// row, lane l accumulates entries l, l+ws, ...; pairwise tree over all ws
+// lanes with ascending strides.
+__global__ void csr_vector_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ v, const double* __restrict__ x,
+                                  double* __restrict__ y, int64_t nrows, int32_t ws, const int* done) {
+    extern __shared__ double part[];
+    if (done && *done) return;
+    const int32_t tid = threadIdx.x;
+    const int32_t lane = tid % ws;
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / ws) + tid / ws;
+    double p = 0.0;
+    if (row < nrows) {
+        const int64_t lo = ro[row], hi = ro[row + 1];
+        for (int64_t k = lo + lane; k < hi; k += ws) p = madd(p, v[k], __ldg(x + ci[k]));
+    }
+    part[tid] = p;
+    for (int32_t st = 1; st < ws; st <<= 1) {
+        __syncthreads();
+        if ((lane & (2 * st - 1)) == 0) part[tid] = __dadd_rn(part[tid], part[tid + st]);
+    }
+    __syncthreads();
+    if (lane == 0 && row < nrows) y[row] = part[tid];
+}
+
+// COO pass (formats.cpp:101-175), step 1: every chunk of ws entries runs the
+// intra-warp segmented inclusive scan keyed on row (Hillis-Steele, ascending
+// strides). Segments that neither continue a carry from the previous chunk
+// nor reach the chunk's last lane are complete: y[row] += total directly.
+// The rest are recorded for the carry chains of step 2.
+struct CooChunkOut {
+    double* tail_val;  // partial sum of the segment ending at the last lane
+    double* head_val;  // total of the first segment, when it carries in and ends inside
+    int32_t* whole;    // the chunk is one row (head segment == tail segment)
+};
+
+__global__ void coo_chunk_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                 const double* __restrict__ vals, int64_t nnz, int32_t ws,
+                                 const double* __restrict__ x, double* __restrict__ y, CooChunkOut out,
+                                 const int* done) {
+    extern __shared__ double smem[];
+    double* sp = smem;
+    int32_t* sr = reinterpret_cast<int32_t*>(smem + blockDim.x);
+    if (done && *done) return;
+    const int32_t tid = threadIdx.x;
+    const int32_t lane = tid % ws;
+    const int64_t chunk = blockIdx.x * (int64_t)(blockDim.x / ws) + tid / ws;
+    const int64_t base = chunk * ws;
+    const int64_t lanes64 = base < nnz ? (nnz - base < ws ? nnz - base : ws) : 0;
+    const int32_t lanes = static_cast<int32_t>(lanes64);
+    const bool live = lane < lanes;
+    double p = live ? __dmul_rn(vals[base + lane], __ldg(x + cols[base + lane])) : 0.0;
+    int32_t r = live ? rows[base + lane] : -1;
+    sp[tid] = p;
+    sr[tid] = r;
+    for (int32_t st = 1; st < ws; st <<= 1) {
+        __syncthreads();
+        const bool take = live && lane >= st && sr[tid - st] == r;
+        const double prev = take ? sp[tid - st] : 0.0;
+        __syncthreads();
+        if (take) {
+            p = __dadd_rn(p, prev);
+            sp[tid] = p;
+        }
+    }
+    __syncthreads();
+    if (!live) return;
+    const bool carry_in = base > 0 && rows[base - 1] == sr[tid - lane];
+    const bool in_head = sr[tid - lane] == r;  // same row as lane 0 => head segment (rows sorted)
+    const bool last = lane + 1 == lanes;
+    const bool end = last || sr[tid + 1] != r;
+    if (last) {
+        out.tail_val[chunk] = p;
+        out.whole[chunk] = in_head ? 1 : 0;
+    } else if (end) {
+        if (in_head && carry_in)
+            out.head_val[chunk] = p;
+        else
+            y[r] = __dadd_rn(y[r], p);
+    }
+}
+
+// COO pass, step 2: one thread per chunk whose tail segment starts a carry
+// chain walks forward exactly as the sequential reference carries it:
+// carry = partial + carry across whole-row chunks, then y[r] += (head + carry)
+// where the row ends, or y[r] += carry when the next chunk starts a new row.
+__global__ void coo_chain_kernel(const int32_t* __restrict__ rows, int64_t nnz, int32_t ws, int64_t nchunks,
+                                 CooChunkOut in, double* __restrict__ y, const int* done) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nchunks || (done && *done)) return;
+    const int64_t base = c * ws;
+    const bool carry_in = c > 0 && rows[base - 1] == rows[base];
+    if (in.whole[c] && carry_in) return;  // continues an earlier chain
+    const int64_t last = base + ws < nnz ? base + ws - 1 : nnz - 1;
+    const int32_t r = rows[last];
+    double carry = in.tail_val[c];
+    for (int64_t k = c + 1;; ++k) {
+        if (k == nchunks || rows[k * ws] != r) {
+            y[r] = __dadd_rn(y[r], carry);
+            return;
+        }
+        if (in.whole[k]) {
+            carry = __dadd_rn(in.tail_val[k], carry);
+            continue;
+        }
+        y[r] = __dadd_rn(y[r], __dadd_rn(in.head_val[k], carry));
+        return;
+    }
+}
+
+// HYB tail: entries beyond the first k_ell of each row, in CSR order.
+__global__ void hyb_tail_count_kernel(const int64_t* __restrict__ ro, int64_t n, int64_t k_ell,
+                                      int64_t* __restrict__ cnt) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t len = ro[r + 1] - ro[r];
+    cnt[r] = len > k_ell ? len - k_ell : 0;
+}
+
+__global__ void hyb_tail_fill_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                     const double* __restrict__ v, const int64_t* __restrict__ start, int64_t n,
+                                     int64_t k_ell, int32_t* __restrict__ trow, int32_t* __restrict__ tcol,
+                                     double* __restrict__ tval) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int64_t o = start[r];
+    for (int64_t k = ro[r] + k_ell; k < ro[r + 1]; ++k, ++o) {
+        trow[o] = static_cast<int32_t>(r);
+        tcol[o] = ci[k];
+        tval[o] = v[k];
+    }
+}
+
+__global__ void expand_rows_kernel(const int64_t* __restrict__ ro, int64_t n, int32_t* __restrict__ rows) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    for (int64_t k = ro[r]; k < ro[r + 1]; ++k) rows[k] = static_cast<int32_t>(r);
+}
+
+__global__ void len_histogram_kernel(const int64_t* __restrict__ ro, int64_t n, unsigned long long* hist) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) atomicAdd(hist + (ro[r + 1] - ro[r]), 1ull);
+}
+
+__global__ void exclusive_scan_small_kernel(const int64_t* in, int64_t* out, int64_t n) {
+    // single-thread scan; only used when the CUB path is not worth a launch
+    int64_t acc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        out[i] = acc;
+        acc += in[i];
+    }
+}
+
+int32_t cta_threads(int32_t ws) { return ws > 256 ? ws : 256; }
+
+}  // namespace
+
+// hyb_default_k_ell (formats.cpp:54-62): the smallest width covering at
+// least 2/3 of the rows, from a device histogram of row lengths.
+int64_t hyb_default_k_ell(const CsrData& m, cudaStream_t s) {
+    if (m.nrows == 0) return 0;
+    const int64_t bins = int64_t(m.maxrow) + 1;
+    Scratch<unsigned long long> hist(bins, s);
+    EW_CUDA_CHECK(cudaMemsetAsync(hist.get(), 0, bins * sizeof(unsigned long long), s));
+    len_histogram_kernel<<<grid_for(m.nrows), kBlock, 0, s>>>(m.ro.get(), m.nrows, hist.get());
+    launched("len_histogram_kernel");
+    std::vector<unsigned long long> h(bins);
+    EW_CUDA_CHECK(cudaMemcpyAsync(h.data(), hist.get(), bins * 8, cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    const double want_d = std::ceil((2.0 / 3.0) * static_cast<double>(m.nrows));
+    int64_t want = static_cast<int64_t>(want_d);
+    want = std::min<int64_t>(std::max<int64_t>(want, 1), m.nrows);
+    unsigned long long acc = 0;
+    for (int64_t L = 0; L < bins; ++L) {
+        acc += h[L];
+        if (static_cast<int64_t>(acc) >= want) return L;  // lengths[want - 1] of the sorted list
+    }
+    return m.maxrow;
+}
+
+std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
+                                         cudaStream_t s) {
+    auto f = std::make_shared<FormatData>();
+    f->ws = ws;
+    f->nrows = m.nrows;
+    f->ncols = m.ncols;
+    f->csr = nullptr;
+    const int64_t n = m.nrows;
+    if (id == "csr_vector" || id == "coo") {
+        f->kind = id == "coo" ? FormatData::kCoo : FormatData::kCsrVector;
+        f->stored_slots = m.nnz;
+        if (f->kind == FormatData::kCoo) {
+            f->coo_nnz = m.nnz;
+            f->coo_rows.alloc(m.nnz);
+            if (n) {
+                expand_rows_kernel<<<grid_for(n), kBlock, 0, s>>>(m.ro.get(), n, f->coo_rows.get());
+                launched("expand_rows_kernel");
+            }
+        }
+        return f;
+    }
+    require(id == "ell" || id == "hyb", "unknown format id");
+    f->kind = id == "ell" ? FormatData::kEll : FormatData::kHyb;
+    int64_t width = m.maxrow;
+    if (f->kind == FormatData::kHyb) {
+        const int64_t k = hyb_k_ell >= 0 ? hyb_k_ell : hyb_default_k_ell(m, s);
+        f->k_ell = k;
+        width = std::min<int64_t>(k, m.maxrow);
+    }
+    f->width = width;
+    f->ell_v.alloc(n * width);
+    f->ell_c.alloc(n * width);
+    if (n && width) {
+        ell_build_kernel<<<grid_for(n), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), n, width,
+                                                        f->ell_v.get(), f->ell_c.get());
+        launched("ell_build_kernel");
+    }
+    f->stored_slots = n * width;
+    if (f->kind == FormatData::kHyb) {
+        Scratch<int64_t> cnt(n + 1, s), start(n + 1, s);
+        if (n) {
+            hyb_tail_count_kernel<<<grid_for(n), kBlock, 0, s>>>(m.ro.get(), n, f->k_ell, cnt.get());
+            launched("hyb_tail_count_kernel");
+            EW_CUDA_CHECK(cudaMemsetAsync(cnt.get() + n, 0, sizeof(int64_t), s));
+            exclusive_scan_small_kernel<<<1, 1, 0, s>>>(cnt.get(), start.get(), n + 1);
+            launched("exclusive_scan_small_kernel");
+        }
+        int64_t tail = 0;
+        if (n) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(&tail, start.get() + n, 8, cudaMemcpyDeviceToHost, s));
+            EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        f->coo_nnz = tail;
+        f->coo_rows.alloc(tail);
+        f->coo_cols.alloc(tail);
+        f->coo_vals.alloc(tail);
+        if (tail) {
+            hyb_tail_fill_kernel<<<grid_for(n), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), start.get(), n,
+                                                                f->k_ell, f->coo_rows.get(), f->coo_cols.get(),
+                                                                f->coo_vals.get());
+            launched("hyb_tail_fill_kernel");
+        }
+        f->stored_slots += tail;
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    return f;
+}
+
+static void coo_pass(const int32_t* rows, const int32_t* cols, const double* vals, int64_t nnz, int32_t ws,
+                     const double* x, double* y, cudaStream_t s, const int* done) {
+    if (nnz == 0) return;
+    const int64_t nchunks = (nnz + ws - 1) / ws;
+    Scratch<double> tail(nchunks, s), head(nchunks, s);
+    Scratch<int32_t> whole(nchunks, s);
+    CooChunkOut o{tail.get(), head.get(), whole.get()};
+    const int32_t T = cta_threads(ws);
+    const int64_t per = T / ws;
+    const unsigned grid = static_cast<unsigned>((nchunks + per - 1) / per);
+    coo_chunk_kernel<<<grid, T, T * (sizeof(double) + sizeof(int32_t)), s>>>(rows, cols, vals, nnz, ws, x, y, o,
+                                                                               done);
+    launched("coo_chunk_kernel");
+    coo_chain_kernel<<<grid_for(nchunks), kBlock, 0, s>>>(rows, nnz, ws, nchunks, o, y, done);
+    launched("coo_chain_kernel");
+}
+
+void format_spmv(const FormatData& f, const CsrData& m, const double* x, double* y, cudaStream_t s,
+                 const int* done) {
+    const int64_t n = f.nrows;
+    if (n == 0) return;
+    switch (f.kind) {
+        case FormatData::kCsrVector: {
+            const int32_t T = cta_threads(f.ws);
+            const int64_t per = T / f.ws;
+            csr_vector_kernel<<<static_cast<unsigned>((n + per - 1) / per), T, T * sizeof(double), s>>>(
+                m.ro.get(), m.ci.get(), m.v.get(), x, y, n, f.ws, done);
+            launched("csr_vector_kernel");
+            return;
+        }
+        case FormatData::kCoo:
+            EW_CUDA_CHECK(cudaMemsetAsync(y, 0, n * sizeof(double), s));
+            coo_pass(f.coo_rows.get(), m.ci.get(), m.v.get(), f.coo_nnz, f.ws, x, y, s, done);
+            return;
+        case FormatData::kEll:
+        case FormatData::kHyb:
+            ell_spmv_kernel<<<grid_for(n), kBlock, 0, s>>>(f.ell_v.get(), f.ell_c.get(), n, f.width, x, y, done);
+            launched("ell_spmv_kernel");
+            if (f.kind == FormatData::kHyb)
+                coo_pass(f.coo_rows.get(), f.coo_cols.get(), f.coo_vals.get(), f.coo_nnz, f.ws, x, y, s, done);
+            return;
+    }
+}
+
+}  // namespace ew

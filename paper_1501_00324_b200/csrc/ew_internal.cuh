@@ -137,13 +137,36 @@ struct LayoutData {
     }
 };
 
+// The paper's comparison formats (formats.hpp:11-53): csr_vector and coo run
+// on the CSR arrays, ell / hyb on their own padded column-major slabs.
+struct FormatData {
+    enum Kind { kCsrVector, kCoo, kEll, kHyb } kind = kCsrVector;
+    int32_t ws = 32;
+    int64_t nrows = 0, ncols = 0, width = 0, k_ell = 0, coo_nnz = 0, stored_slots = 0;
+    const CsrData* csr = nullptr;
+    DevBuf<double> ell_v;
+    DevBuf<int32_t> ell_c;
+    DevBuf<int32_t> coo_rows, coo_cols;  // coo: rows only (cols/vals are the CSR's)
+    DevBuf<double> coo_vals;
+    size_t device_bytes() const {
+        return ell_v.bytes() + ell_c.bytes() + coo_rows.bytes() + coo_cols.bytes() + coo_vals.bytes();
+    }
+};
+
 struct KernelData {
     std::string id;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored_slots = 0;
     bool reordered = false;  // r / rs variants: perm set, apply permutes in/out
-    std::shared_ptr<CsrData> csr;        // csr_ref
+    std::shared_ptr<CsrData> csr;        // csr_ref, and the arrays of csr_vector / coo
     std::shared_ptr<LayoutData> layout;  // k1* / k2*
+    std::shared_ptr<FormatData> format;  // csr_vector / coo / ell / hyb
 };
+
+std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
+                                         cudaStream_t s);
+void format_spmv(const FormatData& f, const CsrData& m, const double* x, double* y, cudaStream_t s,
+                 const int* done);
+int64_t hyb_default_k_ell(const CsrData& m, cudaStream_t s);
 
 // ---- internal API across translation units ---------------------------------
 void validate_config(const ew_warp_config& c);
@@ -151,6 +174,7 @@ std::shared_ptr<CsrData> csr_upload(int64_t nrows, int64_t ncols, int64_t n_ro, 
                                     int64_t nnz, const int64_t* ci, const double* v,
                                     ew_mem_kind mem, bool canonical, cudaStream_t s);
 void csr_spmv(const CsrData& m, const double* x, double* y, cudaStream_t s);
+std::shared_ptr<CsrData> csr_clone(const CsrData& m, cudaStream_t s);
 void csr_diagonal(const CsrData& m, double* d, cudaStream_t s);
 void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
                     cudaStream_t s, unsigned long long* n_active_counter);

@@ -6,6 +6,11 @@ namespace ew {
 
 void kernel_apply(const KernelData& k, const double* x, double* y, bool permuted, cudaStream_t s,
                   const int* done) {
+    if (k.format) {
+        require(!permuted, "kernel '" + k.id + "' has no apply_permuted");
+        format_spmv(*k.format, *k.csr, x, y, s, done);
+        return;
+    }
     if (k.csr) {
         require(!permuted, "kernel '" + k.id + "' has no apply_permuted");
         csr_spmv_guarded(*k.csr, x, y, s, done);
