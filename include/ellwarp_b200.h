@@ -272,6 +272,50 @@ ew_status ew_cg_solve_operator(ew_operator_fn op, void* ctx, ew_mem_kind op_mem,
                                const double* diag, int64_t n, const ew_cg_config* cfg,
                                ew_mem_kind mem, double* x, double* history, ew_cg_result* result,
                                void* stream);
+/* ---- row-partitioned operator and CG (no reference
+ * counterpart: the reference is single-threaded) -------------------------
+ * Partition: contiguous nnz-balanced row blocks, bounds[g] = first row whose
+ * nnz prefix reaches g * nnz / nparts (bounds has nparts + 1 entries). */
+ew_status ew_partition_rows(const int64_t* row_offsets, int64_t nrows, int32_t nparts, int64_t* bounds);
+/* 128-byte ncclUniqueId for ew_dist_create (broadcast it to every rank). */
+ew_status ew_nccl_unique_id(void* id);
+typedef struct ew_dist_t* ew_dist;
+/* Partitions [first_part, first_part + local_parts) of the square global
+ * host CSR, each with a local operator `kernel_id` (k1, k2, csr_ref or a
+ * baseline; r/rs ids need a square local matrix and are rejected).
+ * nccl_id != NULL: NCCL transport, one partition per process
+ * (local_parts = 1, first_part = rank, nparts = world size).
+ * nccl_id == NULL: every partition in this process on the current device
+ * (first_part = 0, local_parts = nparts), halos as device copies.
+ * bounds may be NULL (ew_partition_rows). */
+ew_status ew_dist_create(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets,
+                         int64_t nnz, const int64_t* col_indices, const double* values,
+                         const int64_t* bounds, int32_t nparts, int32_t first_part,
+                         int32_t local_parts, const void* nccl_id, const char* kernel_id,
+                         const ew_warp_config* cfg, const ew_kernel_options* opts, void* stream,
+                         ew_dist* out);
+/* Scalable constructor (NCCL only): this rank passes just its own row block
+ * [bounds[rank], bounds[rank+1]) of the global matrix, with GLOBAL column
+ * ids (row_offsets starts at 0, nrows_local + 1 entries). Ghost requests are
+ * exchanged over NCCL at setup. */
+ew_status ew_dist_create_block(int64_t nrows_global, int64_t nrows_local, const int64_t* row_offsets,
+                               const int64_t* col_indices, const double* values,
+                               const int64_t* bounds, int32_t nparts, int32_t rank,
+                               const void* nccl_id, const char* kernel_id,
+                               const ew_warp_config* cfg, const ew_kernel_options* opts,
+                               void* stream, ew_dist* out);
+ew_status ew_dist_destroy(ew_dist d);
+/* Row range, ghost count and send count of local partition i. */
+ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* row_begin, int64_t* row_end,
+                           int64_t* nghost, int64_t* nsend);
+/* y = A x on this process's owned rows (concatenated in partition order). */
+ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, void* stream);
+/* cg_solve (cg.cpp:25-104) over the partitioned operator: halo exchange per
+ * SpMV, all-gathered dot products summed in rank order. b, diag, x: owned
+ * rows; history on every rank. */
+ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const ew_cg_config* cfg,
+                           ew_mem_kind mem, double* x, double* history, ew_cg_result* result,
+                           void* stream);
 /* compute_alpha (cg.cpp:121-132); *finite = 0 means infinity. */
 ew_status ew_compute_alpha(double t_reorder, double t_kernel, double t_base, int64_t* alpha,
                            int32_t* finite);

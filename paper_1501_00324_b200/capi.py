@@ -148,6 +148,19 @@ _SIGS = {
     "ew_cg_solve_operator": (C.c_int, [OPERATOR_FN, _vp, C.c_int, _vp, _vp, C.c_int64, C.POINTER(CgConfig),
                                        C.c_int, _vp, _vp, C.POINTER(CgResultC), _vp]),
     "ew_compute_alpha": (C.c_int, [C.c_double, C.c_double, C.c_double, _i64p, C.POINTER(C.c_int32)]),
+    "ew_partition_rows": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp]),
+    "ew_nccl_unique_id": (C.c_int, [_vp]),
+    "ew_dist_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, _vp, C.c_int32,
+                                 C.c_int32, C.c_int32, _vp, C.c_char_p, C.POINTER(WarpConfig),
+                                 C.POINTER(KernelOptions), _vp, C.POINTER(_vp)]),
+    "ew_dist_create_block": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp,
+                                       C.c_char_p, C.POINTER(WarpConfig), C.POINTER(KernelOptions), _vp,
+                                       C.POINTER(_vp)]),
+    "ew_dist_destroy": (C.c_int, [_vp]),
+    "ew_dist_get_info": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, _i64p]),
+    "ew_dist_spmv": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "ew_dist_cg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(CgConfig), C.c_int, _vp, _vp, C.POINTER(CgResultC),
+                                   _vp]),
 }
 
 _lib = None
@@ -561,6 +574,119 @@ def cg_solve_operator(op, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=Tr
                                      EW_MEM_HOST, _ptr(x), _ptr(hist), C.byref(res), None))
     return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
                     int(res.spmv_calls))
+
+
+def partition_rows(row_offsets, nparts):
+    """nnz-balanced contiguous row blocks (host rule)."""
+    ro = _host(row_offsets, np.int64)
+    out = np.empty(int(nparts) + 1, np.int64)
+    check(lib().ew_partition_rows(_ptr(ro), ro.size - 1, int(nparts), _ptr(out)))
+    return out
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    check(lib().ew_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class Dist:
+    """Row-partitioned operator + CG (ew_dist).
+
+    Dist.local(...)  -- every partition in this process, on the current GPU
+    Dist.nccl(...)   -- one partition per process from the global CSR
+    Dist.block(...)  -- one partition per process from this rank's row block
+    """
+
+    def __init__(self, h):
+        self.h = h
+        self.owned = 0
+        i = 0
+        while True:
+            r0, r1, ng, ns = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+            if lib().ew_dist_get_info(h, i, C.byref(r0), C.byref(r1), C.byref(ng), C.byref(ns)) != EW_OK:
+                break
+            self.owned += r1.value - r0.value
+            i += 1
+        self.nlocal = i
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.ew_dist_destroy(h)
+            self.h = None
+
+    @staticmethod
+    def _make(m, nparts, first, nlocal, nccl_id, kernel, bounds, warp_size, threshold, stream):
+        ro, ci, v = (_host(m.row_offsets, np.int64), _host(m.col_indices, np.int64), _host(m.values, np.float64))
+        b = _host(bounds, np.int64) if bounds is not None else None
+        cfg = WarpConfig.make(warp_size)
+        opts = KernelOptions(int(threshold), -1)
+        idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        h = C.c_void_p()
+        check(lib().ew_dist_create(m.nrows, m.ncols, ro.size, _ptr(ro), ci.size, _ptr(ci), _ptr(v), _ptr(b),
+                                   int(nparts), int(first), int(nlocal),
+                                   C.cast(idb, C.c_void_p) if idb is not None else None, kernel.encode(),
+                                   C.byref(cfg), C.byref(opts), _stream_ptr(stream), C.byref(h)))
+        return Dist(h)
+
+    @staticmethod
+    def local(m, nparts, kernel="k1", bounds=None, warp_size=32, threshold=0, stream=None):
+        return Dist._make(m, nparts, 0, nparts, None, kernel, bounds, warp_size, threshold, stream)
+
+    @staticmethod
+    def nccl(m, nparts, rank, nccl_id, kernel="k1", bounds=None, warp_size=32, threshold=0, stream=None):
+        return Dist._make(m, nparts, rank, 1, nccl_id, kernel, bounds, warp_size, threshold, stream)
+
+    @staticmethod
+    def block(nglobal, ro, ci, v, bounds, rank, nccl_id, kernel="k1", warp_size=32, threshold=0, stream=None):
+        ro, ci, v = _host(ro, np.int64), _host(ci, np.int64), _host(v, np.float64)
+        b = _host(bounds, np.int64)
+        cfg = WarpConfig.make(warp_size)
+        opts = KernelOptions(int(threshold), -1)
+        idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        check(lib().ew_dist_create_block(int(nglobal), ro.size - 1, _ptr(ro), _ptr(ci), _ptr(v), _ptr(b),
+                                         b.size - 1, int(rank), C.cast(idb, C.c_void_p), kernel.encode(),
+                                         C.byref(cfg), C.byref(opts), _stream_ptr(stream), C.byref(h)))
+        return Dist(h)
+
+    def info(self, i=0):
+        r0, r1, ng, ns = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ew_dist_get_info(self.h, i, C.byref(r0), C.byref(r1), C.byref(ng), C.byref(ns)))
+        return dict(row_begin=r0.value, row_end=r1.value, nghost=ng.value, nsend=ns.value)
+
+    def spmv(self, x, y=None, stream=None):
+        if hasattr(x, "data_ptr"):
+            import torch
+
+            y = torch.empty(self.owned, dtype=torch.float64, device=x.device) if y is None else y
+            check(lib().ew_dist_spmv(self.h, _ptr(x), _ptr(y), EW_MEM_DEVICE, _stream_ptr(stream)))
+            return y
+        xh = _host(x, np.float64)
+        yh = np.empty(self.owned, np.float64)
+        check(lib().ew_dist_spmv(self.h, _ptr(xh), _ptr(yh), EW_MEM_HOST, _stream_ptr(stream)))
+        return yh
+
+    def cg_solve(self, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=True, recompute_interval=50,
+                 divergence_limit=1e6, stream=None):
+        cfg = CgConfig(float(tol), int(max_iterations), 1 if jacobi else 0, int(recompute_interval),
+                       float(divergence_limit))
+        dev = hasattr(b, "data_ptr")
+        if dev:
+            import torch
+
+            x = torch.empty_like(b)
+        else:
+            b = _host(b, np.float64)
+            diag = _host(diag, np.float64) if diag is not None else None
+            x = np.empty(b.size, np.float64)
+        hist = np.empty(int(max_iterations) + 1, np.float64)
+        res = CgResultC()
+        check(lib().ew_dist_cg_solve(self.h, _ptr(b), _ptr(diag), C.byref(cfg), EW_MEM_DEVICE if dev else EW_MEM_HOST,
+                                     _ptr(x), _ptr(hist), C.byref(res), _stream_ptr(stream)))
+        return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
+                        int(res.spmv_calls))
 
 
 def compute_alpha(t_reorder, t_kernel, t_base):

@@ -15,6 +15,9 @@ struct ew_kernel_t {
     std::shared_ptr<ew::KernelData> d;
     ew_layout_t layout_view;
 };
+struct ew_dist_t {
+    std::shared_ptr<ew::DistData> d;
+};
 
 namespace {
 
@@ -383,40 +386,12 @@ ew_status ew_kernel_prepare(const char* id, ew_csr m, const ew_warp_config* cfg,
         ew::require(out != nullptr && id != nullptr, "null argument");
         const ew_warp_config c = cfg ? *cfg : default_config();
         const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
-        ew::validate_config(c);  // prepare_kernel validates first (kernels.cpp:61)
         const std::string sid(id);
-        const int sup = id_support(sid);
-        if (sup < 0) throw ew::Error(EW_INVALID_ARGUMENT, "unknown kernel id '" + sid + "'");
-        if (sup == 0)
-            throw ew::Error(EW_UNSUPPORTED, "kernel '" + sid + "' has no device implementation yet");
-        const auto& src = m->d;
-        auto k = std::make_shared<ew::KernelData>();
-        k->id = sid;
-        k->nrows = src->nrows;
-        k->ncols = src->ncols;
-        k->nnz = src->nnz;
-        k->stored_slots = src->nnz;
-        if (sid == "csr_ref") {
-            k->csr = ew::csr_clone(*src, nullptr);
-        } else if (sid == "csr_vector" || sid == "coo" || sid == "ell" || sid == "hyb") {
-            if (c.warp_size > 1024) throw ew::Error(EW_UNSUPPORTED, "warp_size above 1024 has no device mapping");
-            k->csr = ew::csr_clone(*src, nullptr);
-            k->format = ew::build_format(*src, sid, c.warp_size, o.hyb_k_ell, nullptr);
-            k->stored_slots = k->format->stored_slots;
-        } else {
-            const bool is_k2 = sid[1] == '2';
-            const bool reordered = sid.size() > 2;
-            const int64_t thr = o.k2_threshold > 0 ? o.k2_threshold : std::max<int64_t>(1, src->maxrow);
-            std::shared_ptr<ew::CsrData> op = src;
-            if (reordered) {
-                ew::require(src->nrows == src->ncols, "kernel '" + sid + "' requires a square matrix");
-                op = ew::reorder(*src, nullptr, true, sid.back() == 's' && sid.size() == 4, nullptr, nullptr);
-            }
-            k->reordered = reordered;
-            k->layout = ew::build_layout(*op, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false,
-                                         nullptr);
-            k->stored_slots = k->layout->stored_slots;
+        if (id_support(sid) < 0) {
+            ew::validate_config(c);  // prepare_kernel validates first (kernels.cpp:61)
+            throw ew::Error(EW_INVALID_ARGUMENT, "unknown kernel id '" + sid + "'");
         }
+        auto k = ew::prepare(sid, *m->d, c, o, nullptr);
         auto* h = new ew_kernel_t{std::move(k), ew_layout_t{}};
         h->layout_view.d = h->d->layout;
         *out = h;
@@ -630,6 +605,113 @@ ew_status ew_cg_solve_operator(ew_operator_fn fn, void* ctx, ew_mem_kind op_mem,
     });
     if (pinned) cudaFreeHost(pinned);
     return st;
+}
+
+ew_status ew_partition_rows(const int64_t* row_offsets, int64_t nrows, int32_t nparts, int64_t* bounds) {
+    return guarded([&] {
+        ew::require(row_offsets != nullptr && bounds != nullptr && nrows >= 0, "null argument");
+        const auto b = ew::partition_rows(row_offsets, nrows, nparts);
+        std::copy(b.begin(), b.end(), bounds);
+    });
+}
+
+ew_status ew_nccl_unique_id(void* id) {
+    return guarded([&] {
+        ew::require(id != nullptr, "null argument");
+        ew::nccl_unique_id(id);
+    });
+}
+
+ew_status ew_dist_create(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets, int64_t nnz,
+                         const int64_t* col_indices, const double* values, const int64_t* bounds, int32_t nparts,
+                         int32_t first_part, int32_t local_parts, const void* nccl_id, const char* kernel_id,
+                         const ew_warp_config* cfg, const ew_kernel_options* opts, void* stream, ew_dist* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && row_offsets != nullptr && kernel_id != nullptr, "null argument");
+        ew::require(n_row_offsets == nrows + 1 && row_offsets[nrows] == nnz, "row_offsets length");
+        if (nrows > 0x7fffffff) throw ew::Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        auto d = ew::dist_create(nrows, ncols, row_offsets, col_indices, values, bounds, nparts, first_part,
+                                 local_parts, nccl_id, kernel_id, c, o, ew::as_stream(stream));
+        *out = new ew_dist_t{std::move(d)};
+    });
+}
+
+ew_status ew_dist_create_block(int64_t nrows_global, int64_t nrows_local, const int64_t* row_offsets,
+                               const int64_t* col_indices, const double* values, const int64_t* bounds,
+                               int32_t nparts, int32_t rank, const void* nccl_id, const char* kernel_id,
+                               const ew_warp_config* cfg, const ew_kernel_options* opts, void* stream,
+                               ew_dist* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && row_offsets != nullptr && bounds != nullptr && kernel_id != nullptr,
+                    "null argument");
+        ew::require(rank >= 0 && rank < nparts && bounds[rank + 1] - bounds[rank] == nrows_local,
+                    "block rows do not match the partition bounds");
+        ew::require(row_offsets[0] == 0, "row_offsets[0] != 0");
+        if (nrows_global > 0x7fffffff) throw ew::Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        auto d = ew::dist_create_block(nrows_global, row_offsets, col_indices, values, bounds, nparts, rank, nccl_id,
+                                       kernel_id, c, o, ew::as_stream(stream));
+        *out = new ew_dist_t{std::move(d)};
+    });
+}
+
+ew_status ew_dist_destroy(ew_dist d) {
+    return guarded([&] { delete d; });
+}
+
+ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* r0, int64_t* r1, int64_t* nghost, int64_t* nsend) {
+    return guarded([&] {
+        check_handle(d, "dist");
+        int64_t a = 0, b = 0, c = 0, e = 0;
+        ew::dist_part_info(*d->d, local_index, &a, &b, &c, &e);
+        if (r0) *r0 = a;
+        if (r1) *r1 = b;
+        if (nghost) *nghost = c;
+        if (nsend) *nsend = e;
+    });
+}
+
+ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(d, "dist");
+        const int64_t n = ew::dist_owned_rows(*d->d);
+        with_io(x, n, y, n, mem, ew::as_stream(stream),
+                [&](const double* xd, double* yd) { ew::dist_spmv(*d->d, xd, yd, ew::as_stream(stream)); });
+    });
+}
+
+ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const ew_cg_config* cfg, ew_mem_kind mem,
+                           double* x, double* history, ew_cg_result* result, void* stream) {
+    return guarded([&] {
+        check_handle(d, "dist");
+        ew::require(cfg != nullptr && result != nullptr && b != nullptr && x != nullptr, "null argument");
+        const cudaStream_t s = ew::as_stream(stream);
+        const int64_t n = ew::dist_owned_rows(*d->d);
+        const bool jac = cfg->jacobi != 0;
+        ew::require(!jac || diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+        ew::Scratch<double> bd(mem == EW_MEM_HOST ? n : 0, s), dd(mem == EW_MEM_HOST && jac ? n : 0, s),
+            xd(mem == EW_MEM_HOST ? n : 0, s);
+        const double* bp = b;
+        const double* dp = diag;
+        double* xp = x;
+        if (mem == EW_MEM_HOST) {
+            if (n) {
+                EW_CUDA_CHECK(cudaMemcpyAsync(bd.get(), b, n * 8, cudaMemcpyHostToDevice, s));
+                if (jac) EW_CUDA_CHECK(cudaMemcpyAsync(dd.get(), diag, n * 8, cudaMemcpyHostToDevice, s));
+            }
+            bp = bd.get();
+            dp = jac ? dd.get() : nullptr;
+            xp = xd.get();
+        }
+        ew::CgOutputs o = ew::dist_cg(*d->d, bp, jac ? dp : nullptr, *cfg, xp, s);
+        if (mem == EW_MEM_HOST && n) EW_CUDA_CHECK(cudaMemcpyAsync(x, xd.get(), n * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        *result = o.res;
+        if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+    });
 }
 
 ew_status ew_compute_alpha(double t_reorder, double t_kernel, double t_base, int64_t* alpha, int32_t* finite) {

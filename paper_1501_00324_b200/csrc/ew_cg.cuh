@@ -1,0 +1,290 @@
+// Device kernels of the Jacobi PCG (cg.cpp:25-104), shared by the
+// single-GPU solver (ew_cg.cu) and the row-partitioned one (ew_dist.cu).
+//
+// Every reduction is deterministic: each CTA sums a fixed grid-stride subset
+// of the rows, CTA partials are combined by the last CTA to finish in CTA
+// order. With DIST = false that last CTA also applies the reference's
+// decision (alpha, breakdown, convergence, divergence, beta). With DIST =
+// true it only stores this partition's totals in State::loc; the transport
+// all-gathers them and cg_finalize_kernel sums the partitions in rank order
+// and applies the same decision on every rank.
+#pragma once
+
+#include <cmath>
+
+#include "ew_internal.cuh"
+
+namespace ew {
+namespace cg {
+
+enum Status : int {
+    kRunning = 0,
+    kConverged = 1,
+    kBreakdown = 2,
+    kNonFinite = 3,
+    kDiverged = 4,
+    kBadRhs = 5,
+};
+
+enum What : int { kBnorm = 0, kStart = 1, kPq = 2, kUpdate = 3 };
+
+struct State {
+    double rz, pq, alpha, beta, bnorm, rr, rz_new;
+    int done, status;
+    long long iterations;
+    unsigned int ticket;  // last-CTA election counter
+    int flags;            // bit 0: non-finite residual entry; bit 1: zero diagonal
+    double loc[2];        // DIST: this partition's totals of the current reduction
+};
+
+constexpr int kRedBlock = 256;
+constexpr int kRedGridMax = 148 * 8;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic CTA sum of NV values; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV]) {
+    __shared__ double sh[NV][kRedBlock / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        v[i] = warp_sum(v[i]);
+        if (lane == 0) sh[i][wid] = v[i];
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = warp_sum(lane < kRedBlock / 32 ? sh[i][lane] : 0.0);
+    }
+}
+
+// Publishes this CTA's sums; true in every thread of the last CTA to finish.
+template <int NV>
+__device__ __forceinline__ bool publish_partials(const double (&v)[NV], double* partials, unsigned int* ticket) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) partials[i * gridDim.x + blockIdx.x] = v[i];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    return last;
+}
+
+template <int NV>
+__device__ __forceinline__ void final_sum(double (&out)[NV], const double* partials) {
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+            t = __dadd_rn(t, *((volatile const double*)&partials[i * gridDim.x + b]));
+        v[i] = t;
+    }
+    block_sum<NV>(v);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) out[i] = v[i];
+}
+
+// ---- decisions (cg.cpp), applied to global totals by one thread ----------
+__device__ __forceinline__ void decide_bnorm(State* st, double bb) { st->bnorm = sqrt(bb); }
+
+__device__ __forceinline__ void decide_start(State* st, double rr, double rz, double tol, double* hist) {
+    const double rel = sqrt(rr) / st->bnorm;  // cg.cpp:58
+    hist[0] = rel;
+    st->rz = rz;
+    st->iterations = 0;
+    if (rel <= tol) {
+        st->status = kConverged;
+        st->done = 1;
+    }
+}
+
+__device__ __forceinline__ void decide_pq(State* st, double pq) {
+    st->pq = pq;  // cg.cpp:72-77
+    if (!isfinite(pq) || pq <= 0.0) {
+        st->status = kBreakdown;
+        st->done = 1;
+    } else {
+        st->alpha = st->rz / pq;
+    }
+}
+
+__device__ __forceinline__ void decide_update(State* st, double rr, double rz_new, long long k, double tol,
+                                              double divergence, double* hist) {
+    st->rr = rr;
+    st->rz_new = rz_new;
+    // check_finite(r), cg.cpp:87. A non-finite entry makes r.r non-finite,
+    // which is how the flag reaches every rank of a partitioned solve.
+    if ((st->flags & 1) || !isfinite(rr)) {
+        st->status = kNonFinite;
+        st->done = 1;
+        return;
+    }
+    st->iterations = k;
+    const double rel = sqrt(rr) / st->bnorm;
+    hist[k] = rel;
+    if (rel > divergence) {
+        st->status = kDiverged;
+        st->done = 1;
+        return;
+    }
+    if (rel <= tol) {
+        st->status = kConverged;
+        st->done = 1;
+        return;
+    }
+    st->beta = rz_new / st->rz;
+    st->rz = rz_new;
+}
+
+// Ends a reduction kernel: last CTA either decides (single GPU) or stores
+// the partition's totals (DIST).
+template <bool DIST, int NV, typename Decide>
+__device__ __forceinline__ void finish(const double (&v)[NV], double* partials, State* st, Decide&& decide) {
+    double vv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) vv[i] = v[i];
+    block_sum<NV>(vv);
+    if (!publish_partials<NV>(vv, partials, &st->ticket)) return;
+    double tot[NV];
+    final_sum<NV>(tot, partials);
+    if (threadIdx.x == 0) {
+        st->ticket = 0;
+        if (DIST) {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) st->loc[i] = tot[i];
+        } else {
+            decide(tot);
+        }
+    }
+}
+
+#define EW_GRID_STRIDE(i, n) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ||b||^2 and the pre-checks of cg.cpp:28-33
+template <bool DIST>
+__global__ void __launch_bounds__(kRedBlock) init_kernel(const double* __restrict__ b, const double* __restrict__ diag,
+                                                         int64_t n, int jacobi, double* partials, State* st) {
+    double v[1] = {0.0};
+    int bad_b = 0, zero_d = 0;
+    EW_GRID_STRIDE(i, n) {
+        const double bi = b[i];
+        bad_b |= !isfinite(bi);
+        if (jacobi) zero_d |= diag[i] == 0.0;
+        v[0] = __dadd_rn(v[0], __dmul_rn(bi, bi));
+    }
+    if (bad_b) atomicMax(&st->status, (int)kBadRhs);
+    if (zero_d) atomicOr(&st->flags, 2);
+    finish<DIST, 1>(v, partials, st, [&](const double (&t)[1]) { decide_bnorm(st, t[0]); });
+}
+
+// r = b - A x0, z = r / diag, p = z, r.r and r.z (cg.cpp:50-66)
+template <bool DIST>
+__global__ void __launch_bounds__(kRedBlock) start_kernel(const double* __restrict__ b, const double* __restrict__ diag,
+                                                          const double* __restrict__ ax, double* __restrict__ r,
+                                                          double* __restrict__ p, int64_t n, int jacobi, double tol,
+                                                          double* partials, State* st, double* hist) {
+    double v[2] = {0.0, 0.0};
+    EW_GRID_STRIDE(i, n) {
+        const double ri = __dsub_rn(b[i], ax[i]);
+        r[i] = ri;
+        const double zi = jacobi ? __ddiv_rn(ri, diag[i]) : ri;
+        p[i] = zi;
+        v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
+        v[1] = __dadd_rn(v[1], __dmul_rn(ri, zi));
+    }
+    finish<DIST, 2>(v, partials, st, [&](const double (&t)[2]) { decide_start(st, t[0], t[1], tol, hist); });
+}
+
+// p.q (cg.cpp:72)
+template <bool DIST>
+__global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict__ p, const double* __restrict__ q,
+                                                       int64_t n, double* partials, State* st) {
+    if (st->done) return;
+    double v[1] = {0.0};
+    EW_GRID_STRIDE(i, n) v[0] = __dadd_rn(v[0], __dmul_rn(p[i], q[i]));
+    finish<DIST, 1>(v, partials, st, [&](const double (&t)[1]) { decide_pq(st, t[0]); });
+}
+
+// mode 0: x += alpha p, r -= alpha q, then r.r, r.z   (cg.cpp:78-81, 88-99)
+// mode 1: x += alpha p only (refresh iteration, first half)
+// mode 2: r = b - A x (A x in q), then r.r, r.z       (cg.cpp:82-86)
+template <bool DIST>
+__global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p, const double* __restrict__ q,
+                                                           const double* __restrict__ b,
+                                                           const double* __restrict__ diag, int64_t n, int jacobi,
+                                                           long long k, double tol, double divergence,
+                                                           double* partials, State* st, double* hist) {
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double v[2] = {0.0, 0.0};
+    int bad = 0;
+    EW_GRID_STRIDE(i, n) {
+        if (mode != 2) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        if (mode == 1) continue;
+        const double ri = mode == 0 ? __dsub_rn(r[i], __dmul_rn(alpha, q[i])) : __dsub_rn(b[i], q[i]);
+        r[i] = ri;
+        bad |= !isfinite(ri);
+        const double zi = jacobi ? __ddiv_rn(ri, diag[i]) : ri;
+        v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
+        v[1] = __dadd_rn(v[1], __dmul_rn(ri, zi));
+    }
+    if (mode == 1) return;
+    if (bad) atomicOr(&st->flags, 1);
+    finish<DIST, 2>(v, partials, st, [&](const double (&t)[2]) {
+        decide_update(st, t[0], t[1], k, tol, divergence, hist);
+    });
+}
+
+// p = z + beta p (cg.cpp:96-99)
+static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, const double* __restrict__ r,
+                                                const double* __restrict__ diag, int64_t n, int jacobi,
+                                                const State* st) {
+    if (st->done) return;
+    const double beta = st->beta;
+    EW_GRID_STRIDE(i, n) {
+        const double zi = jacobi ? __ddiv_rn(r[i], diag[i]) : r[i];
+        p[i] = __dadd_rn(zi, __dmul_rn(beta, p[i]));
+    }
+}
+
+// DIST: sum the all-gathered partition totals in rank order, then decide.
+static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, long long k, double tol,
+                                double divergence, State* st, double* hist) {
+    if (what != kBnorm && what != kStart && st->done) return;
+    double t0 = 0.0, t1 = 0.0;
+    for (int g = 0; g < nparts; ++g) {
+        t0 = __dadd_rn(t0, gathered[2 * g]);
+        t1 = __dadd_rn(t1, gathered[2 * g + 1]);
+    }
+    switch (what) {
+        case kBnorm: decide_bnorm(st, t0); break;
+        case kStart: decide_start(st, t0, t1, tol, hist); break;
+        case kPq: decide_pq(st, t0); break;
+        default: decide_update(st, t0, t1, k, tol, divergence, hist); break;
+    }
+}
+
+inline unsigned red_grid(int64_t n) {
+    int64_t g = (n + kRedBlock - 1) / kRedBlock;
+    if (g > kRedGridMax) g = kRedGridMax;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+inline unsigned stream_grid(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+}  // namespace cg
+}  // namespace ew

@@ -1,0 +1,570 @@
+// Row-partitioned SpMV and Jacobi PCG over several GPUs.
+//
+// Partition: contiguous row blocks, nnz-balanced (boundary g is the first
+// row whose nnz prefix reaches g * nnz / G). Each partition keeps its rows
+// with local column numbering: owned columns first (c - r0), then its ghost
+// columns in ascending global id (grouped by owner rank, since owners are
+// contiguous ranges). Per-row entry order is unchanged, so every row sum of
+// the local K1/K2 kernel is the one the single-GPU kernel computes.
+//
+// Per SpMV: pack the owned values peers need (send lists), exchange them
+// into the ghost tail of the extended vector, run the local kernel. Per CG
+// reduction: each partition's totals are all-gathered and summed in rank
+// order on every rank (deterministic, identical decisions everywhere).
+//
+// Transports: NCCL (one process per GPU; ncclSend/Recv inside a group and
+// ncclAllGather on the caller's stream; libnccl is resolved at run time, so
+// the process uses the same NCCL torch.distributed loaded) and an
+// in-process transport that runs all partitions on the current device with
+// device-to-device copies (tests the whole partitioned algorithm on 1 GPU).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "ew_cg.cuh"
+
+namespace ew {
+
+namespace {
+
+// ---- NCCL, resolved at run time -------------------------------------------
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        // prefer the NCCL already mapped into the process (torch's), then the
+        // loader path, then an explicit override
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            if (const char* p = getenv("EW_NCCL_LIBRARY")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h) {
+            err = "libnccl.so.2 not found (load torch.distributed first or set EW_NCCL_LIBRARY)";
+            return;
+        }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    });
+    if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.AllGather)
+        throw Error(EW_UNSUPPORTED, err.empty() ? "NCCL symbols missing" : err);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Error(EW_CUDA, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+
+__global__ void pack_kernel(const int32_t* __restrict__ idx, const double* __restrict__ src, double* __restrict__ dst,
+                            int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) dst[k] = src[idx[k]];
+}
+
+}  // namespace
+
+// ---- the partition plan (host) ---------------------------------------------
+std::vector<int64_t> partition_rows(const int64_t* ro, int64_t nrows, int32_t nparts) {
+    require(nparts >= 1, "partition: need at least one part");
+    std::vector<int64_t> b(static_cast<size_t>(nparts) + 1, nrows);
+    b[0] = 0;
+    const int64_t nnz = ro[nrows];
+    for (int32_t g = 1; g < nparts; ++g) {
+        // first row whose nnz prefix reaches g * nnz / G
+        const int64_t target = static_cast<int64_t>((static_cast<__int128>(nnz) * g) / nparts);
+        const int64_t* it = std::lower_bound(ro, ro + nrows + 1, target);
+        b[g] = std::max<int64_t>(b[g - 1], std::min<int64_t>(nrows, it - ro));
+    }
+    return b;
+}
+
+struct DistPart {
+    int32_t part = 0;
+    int64_t r0 = 0, r1 = 0, nloc = 0, nghost = 0;
+    std::vector<int64_t> recv_off;  // per owner rank, offsets into the ghost tail
+    std::vector<int64_t> send_off;  // per peer rank, offsets into send_idx
+    DevBuf<int32_t> send_idx;       // local owned indices peers need, grouped by peer
+    DevBuf<double> send_buf;
+    std::shared_ptr<CsrData> local;
+    std::shared_ptr<KernelData> op;
+    // CG / SpMV buffers (ext = owned + ghost tail)
+    DevBuf<double> x_ext, p_ext, r, q, b, diag, hist, partials, gathered;
+    DevBuf<cg::State> st;
+};
+
+struct DistData {
+    int32_t nparts = 1, first = 0, nlocal = 1;
+    std::vector<int64_t> bounds;
+    std::vector<std::unique_ptr<DistPart>> parts;  // this process's partitions
+    bool use_nccl = false;
+    ncclComm_t comm = nullptr;
+    std::string kernel_id;
+    ~DistData() {
+        if (comm) nccl().CommDestroy(comm);
+    }
+};
+
+namespace {
+
+// Ghost columns of a row block [r0, r1) given with global column ids:
+// sorted, unique, every column outside the block.
+std::vector<int64_t> ghost_list(const int64_t* bro, const int64_t* bci, int64_t r0, int64_t r1) {
+    std::vector<int64_t> gh;
+    const int64_t nloc = r1 - r0;
+    for (int64_t k = bro[0]; k < bro[nloc]; ++k)
+        if (bci[k] < r0 || bci[k] >= r1) gh.push_back(bci[k]);
+    std::sort(gh.begin(), gh.end());
+    gh.erase(std::unique(gh.begin(), gh.end()), gh.end());
+    return gh;
+}
+
+int32_t owner_of(const std::vector<int64_t>& bounds, int64_t c) {
+    return static_cast<int32_t>(std::upper_bound(bounds.begin(), bounds.end(), c) - bounds.begin() - 1);
+}
+
+// Partition g from its row block (bro: offsets relative to the block,
+// bci: global column ids, bv: values), its ghost list and, per peer, the
+// global ids that peer needs from this partition (ascending).
+void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& bounds, const int64_t* bro,
+                const int64_t* bci, const double* bv, const std::vector<int64_t>& ghosts,
+                const std::vector<std::vector<int64_t>>& peer_needs, const std::string& kid,
+                const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s) {
+    P.part = g;
+    P.r0 = bounds[g];
+    P.r1 = bounds[g + 1];
+    P.nloc = P.r1 - P.r0;
+    P.nghost = static_cast<int64_t>(ghosts.size());
+    P.recv_off.assign(G + 1, 0);
+    for (int64_t c : ghosts) P.recv_off[owner_of(bounds, c) + 1]++;
+    for (int32_t h = 0; h < G; ++h) P.recv_off[h + 1] += P.recv_off[h];
+    std::vector<int32_t> sidx;
+    P.send_off.assign(G + 1, 0);
+    for (int32_t h = 0; h < G; ++h) {
+        for (int64_t c : peer_needs[h]) {
+            require(c >= P.r0 && c < P.r1, "partition: a peer requested a row this partition does not own");
+            sidx.push_back(static_cast<int32_t>(c - P.r0));
+        }
+        P.send_off[h + 1] = static_cast<int64_t>(sidx.size());
+    }
+    // local CSR: owned columns c - r0, ghosts nloc + their position in `ghosts`
+    const int64_t lnnz = bro[P.nloc] - bro[0];
+    std::vector<int64_t> lro(P.nloc + 1), lci(lnnz);
+    for (int64_t r = 0; r <= P.nloc; ++r) lro[r] = bro[r] - bro[0];
+    for (int64_t k = 0; k < lnnz; ++k) {
+        const int64_t c = bci[bro[0] + k];
+        lci[k] = (c >= P.r0 && c < P.r1) ? c - P.r0
+                                         : P.nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), c) - ghosts.begin());
+    }
+    P.local = csr_upload(P.nloc, P.nloc + P.nghost, P.nloc + 1, lro.data(), lnnz, lci.data(), bv + bro[0],
+                         EW_MEM_HOST, false, s);
+    P.op = prepare(kid, *P.local, cfg, opts, s);
+    P.send_idx.alloc(sidx.size());
+    P.send_buf.alloc(sidx.size());
+    if (!sidx.empty())
+        EW_CUDA_CHECK(cudaMemcpyAsync(P.send_idx.get(), sidx.data(), sidx.size() * 4, cudaMemcpyHostToDevice, s));
+    P.x_ext.alloc(P.nloc + P.nghost);
+    P.p_ext.alloc(P.nloc + P.nghost);
+    P.q.alloc(P.nloc);
+    P.gathered.alloc(2 * static_cast<size_t>(G));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// Exchange the owned values peers need into every partition's ghost tail.
+void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+    const int32_t G = D.nparts;
+    if (G == 1) return;
+    for (auto& P : D.parts) {
+        const int64_t ns = static_cast<int64_t>(P->send_idx.size());
+        if (ns) {
+            pack_kernel<<<grid_for(ns), kBlock, 0, s>>>(P->send_idx.get(), ((*P).*ext).get(), P->send_buf.get(), ns);
+            launched("pack_kernel");
+        }
+    }
+    if (D.use_nccl) {
+        DistPart& P = *D.parts[0];
+        const auto& api = nccl();
+        nccl_check(api.GroupStart(), "ncclGroupStart");
+        for (int32_t h = 0; h < G; ++h) {
+            if (h == P.part) continue;
+            const int64_t sc = P.send_off[h + 1] - P.send_off[h];
+            const int64_t rc = P.recv_off[h + 1] - P.recv_off[h];
+            if (sc) nccl_check(api.Send(P.send_buf.get() + P.send_off[h], sc, ncclFloat64, h, D.comm, s), "ncclSend");
+            if (rc)
+                nccl_check(api.Recv((P.*ext).get() + P.nloc + P.recv_off[h], rc, ncclFloat64, h, D.comm, s),
+                           "ncclRecv");
+        }
+        nccl_check(api.GroupEnd(), "ncclGroupEnd");
+        return;
+    }
+    // in-process: partition h's segment for g lands in g's ghost tail
+    for (auto& Pg : D.parts) {
+        for (auto& Ph : D.parts) {
+            if (Ph->part == Pg->part) continue;
+            const int64_t rc = Pg->recv_off[Ph->part + 1] - Pg->recv_off[Ph->part];
+            if (!rc) continue;
+            EW_CUDA_CHECK(cudaMemcpyAsync(((*Pg).*ext).get() + Pg->nloc + Pg->recv_off[Ph->part],
+                                          Ph->send_buf.get() + Ph->send_off[Pg->part], rc * 8,
+                                          cudaMemcpyDeviceToDevice, s));
+        }
+    }
+}
+
+// Every partition's State::loc[0..1] into every partition's `gathered`.
+void allgather(DistData& D, cudaStream_t s) {
+    if (D.use_nccl) {
+        DistPart& P = *D.parts[0];
+        nccl_check(nccl().AllGather(P.st.get()->loc, P.gathered.get(), 2, ncclFloat64, D.comm, s), "ncclAllGather");
+        return;
+    }
+    for (auto& Pg : D.parts)
+        for (auto& Ph : D.parts)
+            EW_CUDA_CHECK(cudaMemcpyAsync(Pg->gathered.get() + 2 * Ph->part, Ph->st.get()->loc, 16,
+                                          cudaMemcpyDeviceToDevice, s));
+}
+
+void finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaStream_t s) {
+    for (auto& P : D.parts) {
+        cg::finalize_kernel<<<1, 1, 0, s>>>(what, P->gathered.get(), D.nparts, k, cfg.rel_tolerance,
+                                            cfg.divergence_limit, P->st.get(), P->hist.get());
+        launched("cg::finalize_kernel");
+    }
+}
+
+void local_spmv(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, bool guard) {
+    for (auto& P : D.parts)
+        kernel_apply(*P->op, ((*P).*ext).get(), P->q.get(), false, s, guard ? &P->st.get()->done : nullptr);
+}
+
+}  // namespace
+
+std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
+                                      const double* v, const int64_t* bounds_in, int32_t nparts, int32_t first,
+                                      int32_t nlocal, const void* nccl_id, const std::string& kid,
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s) {
+    require(nrows == ncols, "partitioned operator must be square");
+    require(nparts >= 1 && first >= 0 && nlocal >= 1 && first + nlocal <= nparts, "bad partition range");
+    require(kid == "k1" || kid == "k2" || kid == "csr_ref" || kid == "csr_vector" || kid == "ell" || kid == "hyb" ||
+                kid == "coo",
+            "partitioned kernels: the local matrix is rectangular (ghost columns), so r/rs ids do not apply");
+    auto D = std::make_shared<DistData>();
+    D->nparts = nparts;
+    D->first = first;
+    D->nlocal = nlocal;
+    D->kernel_id = kid;
+    D->bounds = bounds_in ? std::vector<int64_t>(bounds_in, bounds_in + nparts + 1) : partition_rows(ro, nrows, nparts);
+    require(D->bounds.front() == 0 && D->bounds.back() == nrows, "partition bounds must cover [0, nrows]");
+    for (int32_t g = 0; g < nparts; ++g) require(D->bounds[g] <= D->bounds[g + 1], "partition bounds must be sorted");
+    D->use_nccl = nccl_id != nullptr;
+    if (D->use_nccl) {
+        require(nlocal == 1, "the NCCL transport runs one partition per process");
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        nccl_check(nccl().CommInitRank(&D->comm, nparts, id, first), "ncclCommInitRank");
+    } else {
+        require(nlocal == nparts, "the in-process transport holds every partition");
+    }
+    // every partition's ghost list is computable from the global CSR
+    std::vector<std::vector<int64_t>> ghosts(nparts);
+    for (int32_t h = 0; h < nparts; ++h)
+        ghosts[h] = ghost_list(ro + D->bounds[h], ci, D->bounds[h], D->bounds[h + 1]);
+    for (int32_t g = first; g < first + nlocal; ++g) {
+        std::vector<std::vector<int64_t>> needs(nparts);
+        for (int32_t h = 0; h < nparts; ++h) {
+            if (h == g) continue;
+            for (int64_t c : ghosts[h])
+                if (c >= D->bounds[g] && c < D->bounds[g + 1]) needs[h].push_back(c);
+        }
+        auto P = std::make_unique<DistPart>();
+        build_part(*P, g, nparts, D->bounds, ro + D->bounds[g], ci, v, ghosts[g], needs, kid, cfg, opts, s);
+        D->parts.push_back(std::move(P));
+    }
+    return D;
+}
+
+std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro, const int64_t* bci,
+                                            const double* bv, const int64_t* bounds, int32_t nparts, int32_t rank,
+                                            const void* nccl_id, const std::string& kid, const ew_warp_config& cfg,
+                                            const ew_kernel_options& opts, cudaStream_t s) {
+    require(nccl_id != nullptr, "the block constructor needs the NCCL transport");
+    require(nparts >= 1 && rank >= 0 && rank < nparts, "bad rank");
+    require(kid == "k1" || kid == "k2" || kid == "csr_ref",
+            "partitioned kernels: k1, k2 or csr_ref (the local matrix has ghost columns)");
+    auto D = std::make_shared<DistData>();
+    D->nparts = nparts;
+    D->first = rank;
+    D->nlocal = 1;
+    D->kernel_id = kid;
+    D->bounds.assign(bounds, bounds + nparts + 1);
+    require(D->bounds.front() == 0 && D->bounds.back() == nglobal, "partition bounds must cover [0, nrows]");
+    for (int32_t g = 0; g < nparts; ++g) require(D->bounds[g] <= D->bounds[g + 1], "partition bounds must be sorted");
+    D->use_nccl = true;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    const auto& api = nccl();
+    nccl_check(api.CommInitRank(&D->comm, nparts, id, rank), "ncclCommInitRank");
+    const int64_t r0 = D->bounds[rank], r1 = D->bounds[rank + 1];
+    const std::vector<int64_t> ghosts = ghost_list(bro, bci, r0, r1);
+    // setup exchange: how many ghosts each rank needs from each owner, then
+    // the ghost ids themselves (owner-grouped, ascending)
+    std::vector<int64_t> my_need(nparts, 0);
+    for (int64_t c : ghosts) my_need[owner_of(D->bounds, c)]++;
+    std::vector<std::vector<int64_t>> needs(nparts);
+    {
+        DevBuf<int64_t> dneed(nparts), dall(static_cast<size_t>(nparts) * nparts);
+        EW_CUDA_CHECK(cudaMemcpyAsync(dneed.get(), my_need.data(), nparts * 8, cudaMemcpyHostToDevice, s));
+        nccl_check(api.AllGather(dneed.get(), dall.get(), nparts, ncclInt64, D->comm, s), "ncclAllGather(needs)");
+        std::vector<int64_t> all(static_cast<size_t>(nparts) * nparts);
+        EW_CUDA_CHECK(cudaMemcpyAsync(all.data(), dall.get(), all.size() * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        std::vector<int64_t> goff(nparts + 1, 0);
+        for (int32_t h = 0; h < nparts; ++h) goff[h + 1] = goff[h] + my_need[h];
+        int64_t total_in = 0;
+        for (int32_t h = 0; h < nparts; ++h) total_in += all[static_cast<size_t>(h) * nparts + rank];
+        DevBuf<int64_t> dgh(ghosts.size()), din(total_in);
+        if (!ghosts.empty())
+            EW_CUDA_CHECK(cudaMemcpyAsync(dgh.get(), ghosts.data(), ghosts.size() * 8, cudaMemcpyHostToDevice, s));
+        nccl_check(api.GroupStart(), "ncclGroupStart");
+        int64_t in_off = 0;
+        std::vector<int64_t> ioff(nparts + 1, 0);
+        for (int32_t h = 0; h < nparts; ++h) {
+            const int64_t cnt_in = all[static_cast<size_t>(h) * nparts + rank];
+            ioff[h] = in_off;
+            if (h != rank) {
+                if (my_need[h]) nccl_check(api.Send(dgh.get() + goff[h], my_need[h], ncclInt64, h, D->comm, s), "ncclSend");
+                if (cnt_in) nccl_check(api.Recv(din.get() + in_off, cnt_in, ncclInt64, h, D->comm, s), "ncclRecv");
+            }
+            in_off += cnt_in;
+        }
+        ioff[nparts] = in_off;
+        nccl_check(api.GroupEnd(), "ncclGroupEnd");
+        std::vector<int64_t> hin(total_in);
+        if (total_in) EW_CUDA_CHECK(cudaMemcpyAsync(hin.data(), din.get(), total_in * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int32_t h = 0; h < nparts; ++h)
+            if (h != rank) needs[h].assign(hin.begin() + ioff[h], hin.begin() + ioff[h + 1]);
+    }
+    auto P = std::make_unique<DistPart>();
+    build_part(*P, rank, nparts, D->bounds, bro, bci, bv, ghosts, needs, kid, cfg, opts, s);
+    D->parts.push_back(std::move(P));
+    return D;
+}
+
+int64_t dist_owned_rows(const DistData& D) {
+    int64_t n = 0;
+    for (auto& P : D.parts) n += P->nloc;
+    return n;
+}
+
+void dist_part_info(const DistData& D, int32_t i, int64_t* r0, int64_t* r1, int64_t* nghost, int64_t* nsend) {
+    require(i >= 0 && i < static_cast<int32_t>(D.parts.size()), "no such local partition");
+    const DistPart& P = *D.parts[i];
+    *r0 = P.r0;
+    *r1 = P.r1;
+    *nghost = P.nghost;
+    *nsend = static_cast<int64_t>(P.send_idx.size());
+}
+
+// y = A x over this process's owned rows (device pointers, concatenated in
+// partition order).
+void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s) {
+    int64_t off = 0;
+    for (auto& P : D.parts) {
+        if (P->nloc)
+            EW_CUDA_CHECK(cudaMemcpyAsync(P->x_ext.get(), x + off, P->nloc * 8, cudaMemcpyDeviceToDevice, s));
+        off += P->nloc;
+    }
+    halo(D, &DistPart::x_ext, s);
+    local_spmv(D, &DistPart::x_ext, s, false);
+    off = 0;
+    for (auto& P : D.parts) {
+        if (P->nloc) EW_CUDA_CHECK(cudaMemcpyAsync(y + off, P->q.get(), P->nloc * 8, cudaMemcpyDeviceToDevice, s));
+        off += P->nloc;
+    }
+}
+
+CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_config& cfg, double* x,
+                  cudaStream_t s) {
+    require(cfg.rel_tolerance > 0.0, "cg: tolerance must be positive");
+    require(cfg.max_iterations >= 0, "cg: max_iterations must be >= 0");
+    const int jacobi = cfg.jacobi ? 1 : 0;
+    if (jacobi) require(diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+    int64_t off = 0;
+    for (auto& P : D.parts) {
+        const int64_t n = P->nloc, ne = P->nloc + P->nghost;
+        P->r.alloc(n);
+        P->b.alloc(n);
+        P->diag.alloc(jacobi ? n : 0);
+        P->hist.alloc(cfg.max_iterations + 1);
+        P->partials.alloc(2 * cg::kRedGridMax);
+        P->st.alloc(1);
+        EW_CUDA_CHECK(cudaMemsetAsync(P->st.get(), 0, sizeof(cg::State), s));
+        if (ne) {
+            EW_CUDA_CHECK(cudaMemsetAsync(P->x_ext.get(), 0, ne * 8, s));
+            EW_CUDA_CHECK(cudaMemsetAsync(P->p_ext.get(), 0, ne * 8, s));
+        }
+        if (n) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(P->b.get(), b + off, n * 8, cudaMemcpyDeviceToDevice, s));
+            if (jacobi) EW_CUDA_CHECK(cudaMemcpyAsync(P->diag.get(), diag + off, n * 8, cudaMemcpyDeviceToDevice, s));
+        }
+        off += n;
+    }
+    // ||b||, then the global OR of the local pre-check flags (cg.cpp:28-33)
+    for (auto& P : D.parts) {
+        cg::init_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(P->b.get(), P->diag.get(), P->nloc,
+                                                                              jacobi, P->partials.get(), P->st.get());
+        launched("cg::init_kernel<dist>");
+    }
+    allgather(D, s);
+    finalize(D, cg::kBnorm, 0, cfg, s);
+    std::vector<cg::State> hs(D.parts.size());
+    for (size_t i = 0; i < D.parts.size(); ++i)
+        EW_CUDA_CHECK(cudaMemcpyAsync(&hs[i], D.parts[i]->st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    double flags[2] = {0.0, 0.0};
+    for (auto& h : hs) {
+        if (h.status == cg::kBadRhs) flags[0] = 1.0;
+        if (h.flags & 2) flags[1] = 1.0;
+    }
+    if (D.use_nccl) {  // share the flags: all ranks take the same branch
+        DistPart& P = *D.parts[0];
+        EW_CUDA_CHECK(cudaMemcpyAsync(P.st.get()->loc, flags, 16, cudaMemcpyHostToDevice, s));
+        allgather(D, s);
+        std::vector<double> all(2 * static_cast<size_t>(D.nparts));
+        EW_CUDA_CHECK(cudaMemcpyAsync(all.data(), P.gathered.get(), all.size() * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int32_t g = 0; g < D.nparts; ++g) {
+            flags[0] = std::max(flags[0], all[2 * g]);
+            flags[1] = std::max(flags[1], all[2 * g + 1]);
+        }
+    }
+    if (flags[0] != 0.0) throw Error(EW_CG_DIVERGENCE, "cg: non-finite right-hand side");
+    require(flags[1] == 0.0, "cg: zero diagonal entry under jacobi");
+    CgOutputs out;
+    if (hs[0].bnorm == 0.0) {
+        out.res.converged = 1;
+        out.res.history_len = 1;
+        out.history.assign(1, 0.0);
+        cudaMemsetAsync(x, 0, dist_owned_rows(D) * 8, s);
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        return out;
+    }
+    // r = b - A x0 (x0 = 0; the operator still runs, cg.cpp:52-57)
+    local_spmv(D, &DistPart::x_ext, s, false);
+    for (auto& P : D.parts) {
+        cg::start_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
+            P->b.get(), P->diag.get(), P->q.get(), P->r.get(), P->p_ext.get(), P->nloc, jacobi, cfg.rel_tolerance,
+            P->partials.get(), P->st.get(), P->hist.get());
+        launched("cg::start_kernel<dist>");
+    }
+    allgather(D, s);
+    finalize(D, cg::kStart, 0, cfg, s);
+
+    DistPart& P0 = *D.parts[0];
+    cg::State* hst = nullptr;
+    EW_CUDA_CHECK(cudaMallocHost(&hst, 2 * sizeof(cg::State)));
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+        if (ev[0]) cudaEventDestroy(ev[0]);
+        if (ev[1]) cudaEventDestroy(ev[1]);
+        cudaFreeHost(hst);
+    };
+    cg::State h{};
+    try {
+        EW_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        EW_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        int64_t it = 1;
+        int batch = 8, j = 0;
+        while (it <= cfg.max_iterations) {
+            const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
+            for (; it <= last; ++it) {
+                halo(D, &DistPart::p_ext, s);
+                local_spmv(D, &DistPart::p_ext, s, true);
+                for (auto& P : D.parts) {
+                    cg::pq_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
+                        P->p_ext.get(), P->q.get(), P->nloc, P->partials.get(), P->st.get());
+                    launched("cg::pq_kernel<dist>");
+                }
+                allgather(D, s);
+                finalize(D, cg::kPq, it, cfg, s);
+                const bool refresh = cfg.recompute_interval > 0 && it % cfg.recompute_interval == 0;
+                for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
+                    if (mode < 0) break;
+                    if (mode == 2) {
+                        halo(D, &DistPart::x_ext, s);
+                        local_spmv(D, &DistPart::x_ext, s, true);
+                    }
+                    for (auto& P : D.parts) {
+                        cg::update_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
+                            mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
+                            P->nloc, jacobi, it, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(),
+                            P->st.get(), P->hist.get());
+                        launched("cg::update_kernel<dist>");
+                    }
+                }
+                allgather(D, s);
+                finalize(D, cg::kUpdate, it, cfg, s);
+                for (auto& P : D.parts) {
+                    cg::p_kernel<<<cg::stream_grid(P->nloc), 256, 0, s>>>(P->p_ext.get(), P->r.get(), P->diag.get(),
+                                                                          P->nloc, jacobi, P->st.get());
+                    launched("cg::p_kernel");
+                }
+            }
+            const int slot = j & 1;
+            EW_CUDA_CHECK(cudaMemcpyAsync(&hst[slot], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+            EW_CUDA_CHECK(cudaEventRecord(ev[slot], s));
+            if (j > 0) {
+                EW_CUDA_CHECK(cudaEventSynchronize(ev[slot ^ 1]));
+                if (hst[slot ^ 1].done) break;
+            }
+            ++j;
+            batch = std::min(batch * 2, 64);
+        }
+        EW_CUDA_CHECK(cudaMemcpyAsync(&hst[0], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        h = hst[0];
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+    off = 0;
+    for (auto& P : D.parts) {
+        if (P->nloc) EW_CUDA_CHECK(cudaMemcpyAsync(x + off, P->x_ext.get(), P->nloc * 8, cudaMemcpyDeviceToDevice, s));
+        off += P->nloc;
+    }
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    return cg_outputs(h.status, h.iterations, cfg, P0.hist.get());
+}
+
+void nccl_unique_id(void* out) {
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+}
+
+}  // namespace ew

@@ -196,6 +196,10 @@ int64_t compute_k2_lanes(int64_t nnz_row, int64_t threshold, int64_t warp_size);
 void gather(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s);
 void scatter(const int32_t* idx, const double* in, double* out, int64_t n, cudaStream_t s);
 
+// prepare_kernel (kernels.cpp:59-125) on device data.
+std::shared_ptr<KernelData> prepare(const std::string& id, const CsrData& m, const ew_warp_config& c,
+                                    const ew_kernel_options& o, cudaStream_t s);
+
 // Kernel-level operator: y = A x in the kernel's "apply" (original) or
 // "apply_permuted" (sorted) numbering; device pointers.
 void kernel_apply(const KernelData& k, const double* x, double* y, bool permuted,
@@ -229,6 +233,26 @@ struct KernelOperator final : CgOperator {
 // Device CG. b, diag, x are device pointers in the operator's numbering.
 CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, int64_t n,
                     const ew_cg_config& cfg, double* x, cudaStream_t s);
+// ---- row-partitioned operator / CG (ew_dist.cu) ----
+struct DistData;
+std::vector<int64_t> partition_rows(const int64_t* ro, int64_t nrows, int32_t nparts);
+std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
+                                      const double* v, const int64_t* bounds, int32_t nparts, int32_t first,
+                                      int32_t nlocal, const void* nccl_id, const std::string& kid,
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s);
+std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro, const int64_t* bci,
+                                            const double* bv, const int64_t* bounds, int32_t nparts, int32_t rank,
+                                            const void* nccl_id, const std::string& kid, const ew_warp_config& cfg,
+                                            const ew_kernel_options& opts, cudaStream_t s);
+int64_t dist_owned_rows(const DistData& D);
+void dist_part_info(const DistData& D, int32_t i, int64_t* r0, int64_t* r1, int64_t* nghost, int64_t* nsend);
+void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s);
+CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_config& cfg, double* x,
+                  cudaStream_t s);
+void nccl_unique_id(void* out);
+
+// Final status -> exception or result (+ history copied back).
+CgOutputs cg_outputs(int status, long long iterations, const ew_cg_config& cfg, const double* hist_dev);
 
 constexpr int kBlock = 256;
 inline unsigned grid_for(int64_t n, int block = kBlock) {

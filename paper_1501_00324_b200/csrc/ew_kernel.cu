@@ -4,6 +4,41 @@
 
 namespace ew {
 
+std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, const ew_warp_config& c,
+                                    const ew_kernel_options& o, cudaStream_t s) {
+    validate_config(c);  // prepare_kernel validates first (kernels.cpp:61)
+    auto k = std::make_shared<KernelData>();
+    k->id = sid;
+    k->nrows = src.nrows;
+    k->ncols = src.ncols;
+    k->nnz = src.nnz;
+    k->stored_slots = src.nnz;
+    if (sid == "csr_ref") {
+        k->csr = csr_clone(src, s);  // the closure owns a copy (kernels.cpp:65-68)
+    } else if (sid == "csr_vector" || sid == "coo" || sid == "ell" || sid == "hyb") {
+        if (c.warp_size > 1024) throw Error(EW_UNSUPPORTED, "warp_size above 1024 has no device mapping");
+        k->csr = csr_clone(src, s);
+        k->format = build_format(src, sid, c.warp_size, o.hyb_k_ell, s);
+        k->stored_slots = k->format->stored_slots;
+    } else if (sid == "k1" || sid == "k2" || sid == "k1r" || sid == "k1rs" || sid == "k2r" || sid == "k2rs") {
+        const bool is_k2 = sid[1] == '2';
+        const bool reordered = sid.size() > 2;
+        // KernelOptions::k2_threshold <= 0: the max row length (kernels.cpp:16-21)
+        const int64_t thr = o.k2_threshold > 0 ? o.k2_threshold : std::max<int64_t>(1, src.maxrow);
+        std::shared_ptr<CsrData> op;
+        if (reordered) {
+            require(src.nrows == src.ncols, "kernel '" + sid + "' requires a square matrix");
+            op = reorder(src, nullptr, true, sid.size() == 4, nullptr, s);
+        }
+        k->reordered = reordered;
+        k->layout = build_layout(reordered ? *op : src, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false, s);
+        k->stored_slots = k->layout->stored_slots;
+    } else {
+        throw Error(EW_INVALID_ARGUMENT, "unknown kernel id '" + sid + "'");
+    }
+    return k;
+}
+
 void kernel_apply(const KernelData& k, const double* x, double* y, bool permuted, cudaStream_t s,
                   const int* done) {
     if (k.format) {
