@@ -194,9 +194,49 @@ def reference_cg_rate(n, nc, ro, ci, v, iters):
 
 
 # ---------------------------------------------------------------------------
+# multi-GPU: one z-slab row block of the elasticity box per rank
+# ---------------------------------------------------------------------------
+def build_slab(args, rank, world):
+    """Rank `rank`'s rows of a box(86, 86, 87*world - 1) elasticity mesh: every
+    rank owns 87 node layers, i.e. a config-2-sized block (weak scaling)."""
+    from paper_1501_00324_b200 import workloads as W
+
+    nx = ny = max(2, int(round(86 * args.scale)))
+    per = nx + 1
+    nz = per * world - 1
+    layers = W.slab_layers(nz, world)
+    t = time.time()
+    rb, ng, ro, ci, v = W.box_rows("elasticity", nx, ny, nz, layers[rank], layers[rank + 1])
+    bounds = np.array([3 * (nx + 1) * (ny + 1) * k for k in layers], np.int64)
+    log(f"[bench] rank {rank}: slab layers [{layers[rank]}, {layers[rank + 1]}) of box({nx},{ny},{nz}): "
+        f"{ro.size - 1} rows, {ro[-1]} nnz, {time.time() - t:.1f}s")
+    return ng, ro, ci, v, bounds
+
+
+def dist_operator(args, rank, world):
+    import torch.distributed as dist
+
+    from paper_1501_00324_b200 import capi
+
+    ng, ro, ci, v, bounds = build_slab(args, rank, world)
+    obj = [capi.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    t = time.time()
+    d = capi.Dist.block(ng, ro, ci, v, bounds, rank, obj[0], kernel=args.kernel if args.kernel in
+                        ("k1", "k2", "csr_ref") else "k1")
+    info = d.info()
+    log(f"[bench] rank {rank}: partitioned operator in {time.time() - t:.2f}s, {info['nghost']} ghosts, "
+        f"{info['nsend']} sent per exchange")
+    return d, ng, ro, ci, v, info
+
+
+# ---------------------------------------------------------------------------
 # GPU arms
 # ---------------------------------------------------------------------------
 def run_spmv(args, rank, world, local):
+    if world > 1:
+        return run_spmv_dist(args, rank, world, local)
     import torch
 
     from paper_1501_00324_b200 import capi
@@ -299,7 +339,116 @@ def run_spmv(args, rank, world, local):
     return out
 
 
+def run_spmv_dist(args, rank, world, local):
+    """Row-partitioned SpMV (halo exchange over NCCL + local K1), weak
+    scaling: each rank owns a config-2-sized slab."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_00324_b200 import capi
+
+    hbm, peak_src = peaks()
+    d, ng, ro, ci, v, info = dist_operator(args, rank, world)
+    nloc, nnz = ro.size - 1, int(ro[-1])
+    x = torch.tensor(np.random.default_rng(1 + rank).uniform(0.1, 1.0, nloc), device="cuda")
+    y = torch.empty(nloc, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        d.spmv(x, y, stream=stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = capi.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            d.spmv(x, y, stream=stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = capi.launch_count() - l0
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    tot = torch.tensor([20.0 * nnz, 12.0 * nnz + 16.0 * nloc, float(nnz)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tot)
+    eff, alg, nnz_all = (float(t) for t in tot.tolist())
+    value = eff / (ms * 1e-3) / 1e9
+    per_gpu_alg = alg / world / (ms * 1e-3) / 1e9
+    return {
+        "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)", "value": round(value, 2), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded structured tet mesh, P1 elasticity element matrices)",
+        "config": {"workload": f"row-partitioned fp64 SpMV, elasticity box slab of 87 node layers per GPU "
+                               f"({nloc} rows/GPU)", "config": "c2-per-gpu", "kernel": "k1",
+                   "partition": "z-slab row blocks, halo exchange ncclSend/Recv + local K1",
+                   "nnz_total": int(nnz_all), "ghosts_rank0": info["nghost"],
+                   "l2": "inputs larger than L2 on every GPU"},
+        "roofline": {"bound": "hbm", "achieved": round(per_gpu_alg, 1), "peak": hbm, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": round(per_gpu_alg / hbm, 4), "traffic": None,
+                     "note": "per-GPU algorithmic bytes / max-over-ranks step time (pack + exchange + SpMV)"},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+
+
+def run_cg_dist(args, rank, world, local):
+    """Row-partitioned Jacobi PCG, 1000 iterations, weak scaling."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1501_00324_b200 import capi
+
+    hbm, peak_src = peaks()
+    d, ng, ro, ci, v, info = dist_operator(args, rank, world)
+    nloc, nnz = ro.size - 1, int(ro[-1])
+    ones = torch.ones(d.owned, dtype=torch.float64, device="cuda")
+    b = d.spmv(ones)  # b = A * 1 (ellwarp_cli.cpp:192-195)
+    # diagonal of the owned rows (global column == global row)
+    rows = np.repeat(np.arange(nloc), np.diff(ro))
+    glob_row = rows + int(info["row_begin"])
+    diag = np.zeros(nloc)
+    hit = ci == glob_row
+    diag[rows[hit]] = v[hit]
+    dd = torch.tensor(diag, device="cuda")
+    iters = args.iterations
+    for _ in range(max(1, args.warmup // 3)):
+        d.cg_solve(b, dd, tol=1e-300, max_iterations=10)
+    torch.cuda.synchronize()
+    barrier(world)
+    l0 = capi.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            res = d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = capi.launch_count() - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    it_s = iters / (ms * 1e-3)
+    tot = torch.tensor([float(nnz), float(nloc)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tot)
+    nnz_all, n_all = (float(t) for t in tot.tolist())
+    b_it = 12 * nnz_all + 104 * n_all + (12 * nnz_all + 24 * n_all) / 50
+    per_gpu = b_it / world * it_s / 1e9
+    return {
+        "metric": "CG iterations/s", "value": round(it_s, 2), "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"row-partitioned Jacobi PCG {iters} it, elasticity box slab of 87 node layers per "
+                               f"GPU ({nloc} rows/GPU, natural ordering)", "config": "c5-weak",
+                   "iterations_per_step": iters, "nrows_total": int(n_all), "nnz_total": int(nnz_all),
+                   "final_residual": float(res.residual_history[-1])},
+        "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": round(per_gpu / hbm, 4), "traffic": None,
+                     "algorithmic_bytes_per_iteration": b_it},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+
+
 def run_cg(args, rank, world, local):
+    if world > 1 or args.config == "c5":
+        return run_cg_dist(args, rank, world, local)
     import torch
 
     from paper_1501_00324_b200 import capi

@@ -176,6 +176,69 @@ def elasticity_box(nx=86, ny=86, nz=86, E=1.0, nu=0.3, sigma=1e-3):
     return _stencil_csr(nx, ny, nz, 3, acc)
 
 
+def _element_matrix(kind, corners, E=1.0, nu=0.3, sigma=1e-3):
+    """Element matrix (4b x 4b) of a unit-cell tet incl. the lumped mass shift."""
+    g, vol = _p1_gradients(np.array(corners, np.float64))
+    if kind == "laplacian":
+        ke = vol * g @ g.T
+        ke[np.arange(4), np.arange(4)] += sigma * vol / 4.0
+        return ke
+    B = _strain_b(g)
+    ke = vol * B.T @ _elastic_d(E, nu) @ B
+    ke[np.arange(12), np.arange(12)] += sigma * vol / 4.0
+    return ke
+
+
+def box_rows(kind, nx, ny, nz, k0=0, k1=None, **kw):
+    """Rows of the node layers [k0, k1) of the `kind` ("laplacian" or
+    "elasticity") operator on box(nx, ny, nz), with GLOBAL column ids: the row
+    block one rank of the partitioned solver owns (slab partition along z).
+    Returns (row_begin, nrows_global, ro, ci, v); box_rows(kind, ..., 0,
+    nz + 1) equals laplacian_box / elasticity_box."""
+    k1 = nz + 1 if k1 is None else k1
+    blk = 1 if kind == "laplacian" else 3
+    n1, n2, n3 = nx + 1, ny + 1, nz + 1
+    nzw = k1 - k0
+    ns = len(_STENCIL)
+    dense = np.zeros((nzw, n2, n1, ns, blk, blk), np.float64)
+    for corners in _tet_corners():
+        ke = _element_matrix(kind, corners, **kw)
+        for a, ca in enumerate(corners):
+            lo, hi = max(k0 - ca[2], 0), min(k1 - ca[2], nz)  # cell layers whose corner a is in the window
+            if lo >= hi:
+                continue
+            tgt = dense[lo + ca[2] - k0:hi + ca[2] - k0, ca[1]:ny + ca[1], ca[0]:nx + ca[0]]
+            for b, cb in enumerate(corners):
+                d = _dir_index(tuple(np.subtract(cb, ca)))
+                tgt[..., d, :, :] += ke[blk * a:blk * (a + 1), blk * b:blk * (b + 1)]
+    nn = nzw * n2 * n1
+    dense = dense.reshape(nn, ns, blk, blk)
+    kk, jj, ii = np.meshgrid(np.arange(k0, k1), np.arange(n2), np.arange(n1), indexing="ij")
+    ii, jj, kk = ii.ravel(), jj.ravel(), kk.ravel()
+    present = np.zeros((nn, ns), bool)
+    offs = np.zeros(ns, np.int64)
+    for d, (di, dj, dk) in enumerate(_STENCIL):
+        present[:, d] = ((ii + di >= 0) & (ii + di < n1) & (jj + dj >= 0) & (jj + dj < n2)
+                         & (kk + dk >= 0) & (kk + dk < n3))
+        offs[d] = (dk * n2 + dj) * n1 + di
+    order = np.argsort(offs, kind="stable")
+    present, offs, dense = present[:, order], offs[order], dense[:, order]
+    node = k0 * n2 * n1 + np.arange(nn, dtype=np.int64)
+    ro = np.zeros(nn * blk + 1, np.int64)
+    np.cumsum(np.repeat(present.sum(axis=1) * blk, blk), out=ro[1:])
+    cols = (node[:, None] + offs[None, :])[:, :, None] * blk + np.arange(blk)[None, None, :]
+    cols = np.broadcast_to(cols[:, None, :, :], (nn, blk, ns, blk))
+    mask = np.broadcast_to(present[:, None, :, None], (nn, blk, ns, blk))
+    ci = cols[mask].astype(np.int64)
+    v = np.transpose(dense, (0, 2, 1, 3))[mask].astype(np.float64)
+    return k0 * n2 * n1 * blk, n1 * n2 * n3 * blk, ro, ci, v
+
+
+def slab_layers(nz, nparts):
+    """Node-layer boundaries of a z-slab partition of box(., ., nz)."""
+    return [round(g * (nz + 1) / nparts) for g in range(nparts + 1)]
+
+
 def _tet_grad_vol(p0, p1, p2, p3):
     """Closed-form P1 gradients (4 x (..., 3)) and volumes of tets whose corner
     coordinates are (..., 3) arrays (element_geometry, fem/element.cpp:7-47)."""
