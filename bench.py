@@ -157,6 +157,17 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
+def sum_over_ranks(vals, world):
+    if world == 1:
+        return [float(x) for x in vals]
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return [float(x) for x in t.tolist()]
+
+
 # ---------------------------------------------------------------------------
 # CPU: the reference (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------
@@ -369,9 +380,7 @@ def run_spmv_dist(args, rank, world, local):
     launches = capi.launch_count() - l0
     barrier(world)
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
-    tot = torch.tensor([20.0 * nnz, 12.0 * nnz + 16.0 * nloc, float(nnz)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(tot)
-    eff, alg, nnz_all = (float(t) for t in tot.tolist())
+    eff, alg, nnz_all = sum_over_ranks([20.0 * nnz, 12.0 * nnz + 16.0 * nloc, float(nnz)], world)
     value = eff / (ms * 1e-3) / 1e9
     per_gpu_alg = alg / world / (ms * 1e-3) / 1e9
     return {
@@ -426,9 +435,7 @@ def run_cg_dist(args, rank, world, local):
     launches = capi.launch_count() - l0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
     it_s = iters / (ms * 1e-3)
-    tot = torch.tensor([float(nnz), float(nloc)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(tot)
-    nnz_all, n_all = (float(t) for t in tot.tolist())
+    nnz_all, n_all = sum_over_ranks([float(nnz), float(nloc)], world)
     b_it = 12 * nnz_all + 104 * n_all + (12 * nnz_all + 24 * n_all) / 50
     per_gpu = b_it / world * it_s / 1e9
     return {

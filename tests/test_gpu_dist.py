@@ -123,7 +123,7 @@ def test_partitioned_cg_long_run_and_errors(ew, R, spd):
     with pytest.raises(ValueError):
         d.cg_solve(b, zd)
     with pytest.raises(ValueError):
-        ew.Dist.local(fem, 2, kernel="k1rs")
+        ew.Dist.local(spd, 2, kernel="k1rs")
 
 
 def _nccl_world1():
