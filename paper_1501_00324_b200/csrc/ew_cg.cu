@@ -86,9 +86,11 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
                     stop = true;
                     break;
                 }
-                op.apply(p.get(), q.get(), s, done);
-                cg::pq_kernel<false><<<g, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
-                launched("cg::pq_kernel");
+                if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), st.get(), 0})) {
+                    op.apply(p.get(), q.get(), s, done);
+                    cg::pq_kernel<false><<<g, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
+                    launched("cg::pq_kernel");
+                }
                 const bool refresh = interval > 0 && it % interval == 0;
                 cg::update_kernel<false><<<g, cg::kRedBlock, 0, s>>>(
                     refresh ? 1 : 0, x, r.get(), p.get(), q.get(), b, diag, n, jacobi, it, cfg.rel_tolerance,

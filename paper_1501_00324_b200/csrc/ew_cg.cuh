@@ -204,13 +204,36 @@ __global__ void __launch_bounds__(kRedBlock) start_kernel(const double* __restri
     finish<DIST, 2>(v, partials, st, [&](const double (&t)[2]) { decide_start(st, t[0], t[1], tol, hist); });
 }
 
+// The streaming kernels below take U elements per thread per round (indices
+// i, i+S, ..., i+(U-1)S with S the grid's thread count) and issue every load
+// of a round before the order-preserving arithmetic consumes them: U times
+// the bytes in flight of a plain grid-stride loop, which alone is latency
+// bound at the occupancy these kernels reach.
+constexpr int kU = 4;
+constexpr int kUpdU = 2;  // the update kernel's divisions cost registers: two per round
+#define EW_ROUNDS_U(i0, S, n, U)                                                                 \
+    for (int64_t S = (int64_t)gridDim.x * blockDim.x, i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; \
+         i0 < (n); i0 += (U) * S)
+#define EW_ROUNDS(i0, S, n) EW_ROUNDS_U(i0, S, n, kU)
+
 // p.q (cg.cpp:72)
 template <bool DIST>
 __global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict__ p, const double* __restrict__ q,
                                                        int64_t n, double* partials, State* st) {
     if (st->done) return;
     double v[1] = {0.0};
-    EW_GRID_STRIDE(i, n) v[0] = __dadd_rn(v[0], __dmul_rn(p[i], q[i]));
+    EW_ROUNDS(i0, S, n) {
+        double a[kU], c[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * S;
+            a[u] = i < n ? p[i] : 0.0;
+            c[u] = i < n ? q[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * S < n) v[0] = __dadd_rn(v[0], __dmul_rn(a[u], c[u]));
+    }
     finish<DIST, 1>(v, partials, st, [&](const double (&t)[1]) { decide_pq(st, t[0]); });
 }
 
@@ -228,15 +251,32 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
     const double alpha = st->alpha;
     double v[2] = {0.0, 0.0};
     int bad = 0;
-    EW_GRID_STRIDE(i, n) {
-        if (mode != 2) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-        if (mode == 1) continue;
-        const double ri = mode == 0 ? __dsub_rn(r[i], __dmul_rn(alpha, q[i])) : __dsub_rn(b[i], q[i]);
-        r[i] = ri;
-        bad |= !isfinite(ri);
-        const double zi = jacobi ? __ddiv_rn(ri, diag[i]) : ri;
-        v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
-        v[1] = __dadd_rn(v[1], __dmul_rn(ri, zi));
+    EW_ROUNDS_U(i0, S, n, kUpdU) {
+        double xv[kUpdU], pv[kUpdU], qv[kUpdU], rv[kUpdU], dv[kUpdU];
+#pragma unroll
+        for (int u = 0; u < kUpdU; ++u) {
+            const int64_t i = i0 + u * S;
+            const bool ok = i < n;
+            xv[u] = ok && mode != 2 ? x[i] : 0.0;
+            pv[u] = ok && mode != 2 ? p[i] : 0.0;
+            qv[u] = ok && mode != 1 ? q[i] : 0.0;
+            rv[u] = ok && mode != 1 ? (mode == 0 ? r[i] : b[i]) : 0.0;
+            dv[u] = ok && mode != 1 && jacobi ? diag[i] : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kUpdU; ++u) {
+            const int64_t i = i0 + u * S;
+            if (i >= n) continue;
+            if (mode != 2) x[i] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+            if (mode == 1) continue;
+            // mode 0: r - alpha q; mode 2: b - Ax (rv holds b)
+            const double ri = mode == 0 ? __dsub_rn(rv[u], __dmul_rn(alpha, qv[u])) : __dsub_rn(rv[u], qv[u]);
+            r[i] = ri;
+            bad |= !isfinite(ri);
+            const double zi = jacobi ? __ddiv_rn(ri, dv[u]) : ri;
+            v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
+            v[1] = __dadd_rn(v[1], __dmul_rn(ri, zi));
+        }
     }
     if (mode == 1) return;
     if (bad) atomicOr(&st->flags, 1);
@@ -251,9 +291,23 @@ static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, c
                                                 const State* st) {
     if (st->done) return;
     const double beta = st->beta;
-    EW_GRID_STRIDE(i, n) {
-        const double zi = jacobi ? __ddiv_rn(r[i], diag[i]) : r[i];
-        p[i] = __dadd_rn(zi, __dmul_rn(beta, p[i]));
+    EW_ROUNDS(i0, S, n) {
+        double rv[kU], dv[kU], pv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * S;
+            const bool ok = i < n;
+            rv[u] = ok ? r[i] : 0.0;
+            dv[u] = ok && jacobi ? diag[i] : 1.0;
+            pv[u] = ok ? p[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * S;
+            if (i >= n) continue;
+            const double zi = jacobi ? __ddiv_rn(rv[u], dv[u]) : rv[u];
+            p[i] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
+        }
     }
 }
 

@@ -503,8 +503,12 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
             const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
             for (; it <= last; ++it) {
                 halo(D, &DistPart::p_ext, s);
-                local_spmv(D, &DistPart::p_ext, s, true);
                 for (auto& P : D.parts) {
+                    const int* done = &P->st.get()->done;
+                    if (kernel_apply_dot(*P->op, P->p_ext.get(), P->q.get(), false, s, done,
+                                         DotSink{P->partials.get(), P->st.get(), 1}))
+                        continue;
+                    kernel_apply(*P->op, P->p_ext.get(), P->q.get(), false, s, done);
                     cg::pq_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
                         P->p_ext.get(), P->q.get(), P->nloc, P->partials.get(), P->st.get());
                     launched("cg::pq_kernel<dist>");

@@ -187,6 +187,18 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s);
 std::shared_ptr<LayoutData> import_layout(const ew_layout_desc& d, cudaStream_t s);
+// Where a CG-fused SpMV puts its p.q reduction (ew_spmv.cu k1_dot_kernel).
+namespace cg {
+struct State;
+}
+struct DotSink {
+    double* partials;  // >= cg::kRedGridMax doubles
+    cg::State* st;     // ticket, decision / partition total
+    int dist;          // 1: store the partition total in st->loc
+};
+// K1 SpMV with p.q fused (x is p); false when the layout has no fused path.
+bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
+                     const int* done, const DotSink& sink);
 // done (nullable, device): the launch is a no-op once *done != 0 (CG overrun).
 void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
                  const int* done = nullptr);
@@ -215,9 +227,14 @@ struct CgOutputs {
 // The CG operator: y = A x on device pointers, enqueued on s. A host-callback
 // operator (the reference's arbitrary SpmvFn closure) runs synchronously on
 // the host thread; the solver then checks its done flag before each call.
+bool kernel_apply_dot(const KernelData& k, const double* x, double* y, bool permuted, cudaStream_t s,
+                      const int* done, const DotSink& sink);
+
 struct CgOperator {
     virtual ~CgOperator() = default;
     virtual void apply(const double* x, double* y, cudaStream_t s, const int* done) const = 0;
+    // y = A x with p.q = x.y reduced into `sink`; false: not fused, use apply + a dot kernel
+    virtual bool apply_dot(const double*, double*, cudaStream_t, const int*, const DotSink&) const { return false; }
     virtual bool host_callback() const { return false; }
     virtual int64_t size() const = 0;
 };
@@ -227,6 +244,9 @@ struct KernelOperator final : CgOperator {
     KernelOperator(const KernelData& kd, bool p) : k(kd), permuted(p) {}
     void apply(const double* x, double* y, cudaStream_t s, const int* done) const override {
         kernel_apply(k, x, y, permuted, s, done);
+    }
+    bool apply_dot(const double* x, double* y, cudaStream_t s, const int* done, const DotSink& sink) const override {
+        return kernel_apply_dot(k, x, y, permuted, s, done, sink);
     }
     int64_t size() const override { return k.nrows == k.ncols ? k.nrows : -1; }
 };

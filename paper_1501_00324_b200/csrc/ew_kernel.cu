@@ -39,6 +39,14 @@ std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, 
     return k;
 }
 
+bool kernel_apply_dot(const KernelData& k, const double* x, double* y, bool permuted, cudaStream_t s,
+                      const int* done, const DotSink& sink) {
+    if (!k.layout || k.format) return false;
+    if (!k.reordered) return layout_spmv_dot(*k.layout, x, y, /*scatter=*/true, s, done, sink);
+    if (permuted) return layout_spmv_dot(*k.layout, x, y, /*scatter=*/false, s, done, sink);
+    return false;  // r/rs apply() gathers x first: the dot stays a separate pass
+}
+
 void kernel_apply(const KernelData& k, const double* x, double* y, bool permuted, cudaStream_t s,
                   const int* done) {
     if (k.format) {

@@ -12,7 +12,7 @@
 // included), with the multiply and the add rounded separately (no FMA), and
 // K2 combines lane partials with the reference's ascending-stride pairwise
 // tree (stride 1, 2, 4, ...), done here with __shfl_down_sync.
-#include "ew_internal.cuh"
+#include "ew_cg.cuh"
 
 namespace ew {
 
@@ -126,6 +126,37 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
     a.y[SCATTER ? a.fwd[p] : p] = sum;
 }
 
+// K1 with the CG's p.q fused in (cg.cpp:72): the operator input x is p, so
+// each row adds x[target] * y[target] to a deterministic grid reduction
+// whose last CTA applies the breakdown test and alpha = rz / pq (or, for a
+// partitioned solve, stores the partition total). Grid-stride over rows so
+// the partial count stays at most cg::kRedGridMax.
+template <bool SORTED, bool SCATTER>
+__global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, DotSink sink) {
+    if (a.done && *a.done) return;  // uniform across the grid
+    const uint64_t pol = evict_first_policy();
+    double acc[1] = {0.0};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.nrows;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double sum = 0.0;
+        const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
+        if (active) {
+            const int64_t w = p >> a.ws_log2;
+            const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
+            sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+        }
+        const int64_t t = SCATTER ? a.fwd[p] : p;
+        a.y[t] = sum;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(a.x[t], sum));
+    }
+    cg::State* st = sink.st;
+    if (sink.dist) {
+        cg::finish<true, 1>(acc, sink.partials, st, [](const double (&)[1]) {});
+    } else {
+        cg::finish<false, 1>(acc, sink.partials, st, [&](const double (&tot)[1]) { cg::decide_pq(st, tot[0]); });
+    }
+}
+
 struct K2Args {
     const double* values;
     const int32_t* cols;
@@ -226,6 +257,27 @@ void launch_k2(const K2Args& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
+                     const int* done, const DotSink& sink) {
+    if (l.kind != EW_LAYOUT_K1 || l.row_major || l.nrows == 0) return false;
+    K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
+             l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
+    const unsigned grid = cg::red_grid(l.nrows);
+    if (l.sorted) {
+        if (scatter)
+            k1_dot_kernel<true, true><<<grid, 256, 0, s>>>(a, sink);
+        else
+            k1_dot_kernel<true, false><<<grid, 256, 0, s>>>(a, sink);
+    } else {
+        if (scatter)
+            k1_dot_kernel<false, true><<<grid, 256, 0, s>>>(a, sink);
+        else
+            k1_dot_kernel<false, false><<<grid, 256, 0, s>>>(a, sink);
+    }
+    launched("k1_dot_kernel");
+    return true;
+}
 
 void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
                  const int* done) {
