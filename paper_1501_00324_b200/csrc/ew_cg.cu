@@ -33,7 +33,9 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
     EW_CUDA_CHECK(cudaMemsetAsync(st.get(), 0, sizeof(State), s));
     if (n) EW_CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
     const unsigned g = cg::red_grid(n);
-    const unsigned gs = cg::stream_grid(n);
+    const unsigned gs = cg::resident_grid(cg::p_kernel, 256, n);
+    const unsigned g_pq = cg::resident_grid(cg::pq_kernel<false>, cg::kRedBlock, n);
+    const unsigned g_up = cg::resident_grid(cg::update_kernel<false>, cg::kRedBlock, n);
 
     cg::init_kernel<false><<<g, cg::kRedBlock, 0, s>>>(b, diag, n, jacobi, partials.get(), st.get());
     launched("cg::init_kernel");
@@ -88,17 +90,17 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
                 }
                 if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), st.get(), 0})) {
                     op.apply(p.get(), q.get(), s, done);
-                    cg::pq_kernel<false><<<g, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
+                    cg::pq_kernel<false><<<g_pq, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
                     launched("cg::pq_kernel");
                 }
                 const bool refresh = interval > 0 && it % interval == 0;
-                cg::update_kernel<false><<<g, cg::kRedBlock, 0, s>>>(
+                cg::update_kernel<false><<<g_up, cg::kRedBlock, 0, s>>>(
                     refresh ? 1 : 0, x, r.get(), p.get(), q.get(), b, diag, n, jacobi, it, cfg.rel_tolerance,
                     cfg.divergence_limit, partials.get(), st.get(), hist.get());
                 launched("cg::update_kernel");
                 if (refresh) {
                     if (!(host_op && host_done())) op.apply(x, q.get(), s, done);
-                    cg::update_kernel<false><<<g, cg::kRedBlock, 0, s>>>(
+                    cg::update_kernel<false><<<g_up, cg::kRedBlock, 0, s>>>(
                         2, x, r.get(), p.get(), q.get(), b, diag, n, jacobi, it, cfg.rel_tolerance,
                         cfg.divergence_limit, partials.get(), st.get(), hist.get());
                     launched("cg::update_kernel");

@@ -334,6 +334,28 @@ inline unsigned red_grid(int64_t n) {
     return static_cast<unsigned>(g < 1 ? 1 : g);
 }
 
+// Grid-stride kernels: exactly one wave of resident CTAs (SM count x
+// occupancy), so no partial last wave idles half the GPU; capped by the
+// partial-sum buffer and by the work.
+template <typename Kernel>
+unsigned resident_grid(Kernel kernel, int block, int64_t n) {
+    static thread_local int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    int64_t g = static_cast<int64_t>(sms) * per_sm;
+    if (g > kRedGridMax) g = kRedGridMax;
+    const int64_t need = (n + block - 1) / block;
+    if (g > need) g = need;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
 inline unsigned stream_grid(int64_t n) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;

@@ -523,7 +523,9 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                         local_spmv(D, &DistPart::x_ext, s, true);
                     }
                     for (auto& P : D.parts) {
-                        cg::update_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
+                        cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock,
+                                                                    P->nloc),
+                                                  cg::kRedBlock, 0, s>>>(
                             mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
                             P->nloc, jacobi, it, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(),
                             P->st.get(), P->hist.get());
@@ -533,7 +535,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                 allgather(D, s);
                 finalize(D, cg::kUpdate, it, cfg, s);
                 for (auto& P : D.parts) {
-                    cg::p_kernel<<<cg::stream_grid(P->nloc), 256, 0, s>>>(P->p_ext.get(), P->r.get(), P->diag.get(),
+                    cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, s>>>(P->p_ext.get(), P->r.get(), P->diag.get(),
                                                                           P->nloc, jacobi, P->st.get());
                     launched("cg::p_kernel");
                 }

@@ -263,17 +263,13 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     if (l.kind != EW_LAYOUT_K1 || l.row_major || l.nrows == 0) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
-    const unsigned grid = cg::red_grid(l.nrows);
+    auto go = [&](auto kernel) {
+        kernel<<<cg::resident_grid(kernel, 256, l.nrows), 256, 0, s>>>(a, sink);
+    };
     if (l.sorted) {
-        if (scatter)
-            k1_dot_kernel<true, true><<<grid, 256, 0, s>>>(a, sink);
-        else
-            k1_dot_kernel<true, false><<<grid, 256, 0, s>>>(a, sink);
+        scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
     } else {
-        if (scatter)
-            k1_dot_kernel<false, true><<<grid, 256, 0, s>>>(a, sink);
-        else
-            k1_dot_kernel<false, false><<<grid, 256, 0, s>>>(a, sink);
+        scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
     }
     launched("k1_dot_kernel");
     return true;
