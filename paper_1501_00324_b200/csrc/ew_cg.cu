@@ -28,7 +28,9 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
     require(cfg.max_iterations >= 0, "cg: max_iterations must be >= 0");
 
     DevBuf<double> r(n), p(n), q(n), hist(cfg.max_iterations + 1);
-    DevBuf<double> partials(2 * cg::kRedGridMax);
+    // CG reductions use 2 x kRedGridMax partials; the SpMV-fused p.q one per SpMV CTA
+    const size_t npart = std::max<size_t>(2 * cg::kRedGridMax, static_cast<size_t>((n + 255) / 256));
+    DevBuf<double> partials(npart);
     DevBuf<State> st(1);
     EW_CUDA_CHECK(cudaMemsetAsync(st.get(), 0, sizeof(State), s));
     if (n) EW_CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
@@ -88,7 +90,7 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
                     stop = true;
                     break;
                 }
-                if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), st.get(), 0})) {
+                if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), static_cast<unsigned>(npart), st.get(), 0})) {
                     op.apply(p.get(), q.get(), s, done);
                     cg::pq_kernel<false><<<g_pq, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
                     launched("cg::pq_kernel");

@@ -311,6 +311,31 @@ static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, c
     }
 }
 
+// Ends the SpMV-fused p.q: one CTA sums the per-CTA partials of
+// k1_dot_kernel in a fixed order, then decides (or stores the partition
+// total for a partitioned solve).
+static __global__ void __launch_bounds__(1024) dot_final_kernel(const double* __restrict__ partials, unsigned n,
+                                                                State* st, int dist) {
+    if (st->done) return;
+    __shared__ double sh[32];
+    double t = 0.0;
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) t = __dadd_rn(t, partials[i]);
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        t = warp_sum(threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0);
+        if (threadIdx.x == 0) {
+            if (dist) {
+                st->loc[0] = t;
+                st->loc[1] = 0.0;
+            } else {
+                decide_pq(st, t);
+            }
+        }
+    }
+}
+
 // DIST: sum the all-gathered partition totals in rank order, then decide.
 static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, long long k, double tol,
                                 double divergence, State* st, double* hist) {

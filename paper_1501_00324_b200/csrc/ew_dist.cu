@@ -420,7 +420,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         P->b.alloc(n);
         P->diag.alloc(jacobi ? n : 0);
         P->hist.alloc(cfg.max_iterations + 1);
-        P->partials.alloc(2 * cg::kRedGridMax);
+        P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, static_cast<size_t>((n + 255) / 256)));
         P->st.alloc(1);
         EW_CUDA_CHECK(cudaMemsetAsync(P->st.get(), 0, sizeof(cg::State), s));
         if (ne) {
@@ -506,7 +506,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                 for (auto& P : D.parts) {
                     const int* done = &P->st.get()->done;
                     if (kernel_apply_dot(*P->op, P->p_ext.get(), P->q.get(), false, s, done,
-                                         DotSink{P->partials.get(), P->st.get(), 1}))
+                                         DotSink{P->partials.get(), static_cast<unsigned>(P->partials.size()), P->st.get(), 1}))
                         continue;
                     kernel_apply(*P->op, P->p_ext.get(), P->q.get(), false, s, done);
                     cg::pq_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(

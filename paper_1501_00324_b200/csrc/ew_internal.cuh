@@ -192,9 +192,10 @@ namespace cg {
 struct State;
 }
 struct DotSink {
-    double* partials;  // >= cg::kRedGridMax doubles
-    cg::State* st;     // ticket, decision / partition total
-    int dist;          // 1: store the partition total in st->loc
+    double* partials;   // one partial per SpMV CTA
+    unsigned capacity;  // partials' length; a larger grid falls back to the dot kernel
+    cg::State* st;      // decision / partition total
+    int dist;           // 1: store the partition total in st->loc
 };
 // K1 SpMV with p.q fused (x is p); false when the layout has no fused path.
 bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,

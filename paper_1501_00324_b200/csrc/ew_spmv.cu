@@ -132,12 +132,12 @@ __global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
 // partitioned solve, stores the partition total). Grid-stride over rows so
 // the partial count stays at most cg::kRedGridMax.
 template <bool SORTED, bool SCATTER>
-__global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, DotSink sink) {
+__global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
     if (a.done && *a.done) return;  // uniform across the grid
-    const uint64_t pol = evict_first_policy();
-    double acc[1] = {0.0};
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.nrows;
-         p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double v[1] = {0.0};
+    if (p < a.nrows) {
+        const uint64_t pol = evict_first_policy();
         double sum = 0.0;
         const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
         if (active) {
@@ -147,14 +147,10 @@ __global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, DotSink sink) {
         }
         const int64_t t = SCATTER ? a.fwd[p] : p;
         a.y[t] = sum;
-        acc[0] = __dadd_rn(acc[0], __dmul_rn(a.x[t], sum));
+        v[0] = __dmul_rn(a.x[t], sum);
     }
-    cg::State* st = sink.st;
-    if (sink.dist) {
-        cg::finish<true, 1>(acc, sink.partials, st, [](const double (&)[1]) {});
-    } else {
-        cg::finish<false, 1>(acc, sink.partials, st, [&](const double (&tot)[1]) { cg::decide_pq(st, tot[0]); });
-    }
+    cg::block_sum<1>(v);  // fixed tree; one partial per CTA, summed by cg::dot_final_kernel
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
 }
 
 struct K2Args {
@@ -263,15 +259,17 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     if (l.kind != EW_LAYOUT_K1 || l.row_major || l.nrows == 0) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
-    auto go = [&](auto kernel) {
-        kernel<<<cg::resident_grid(kernel, 256, l.nrows), 256, 0, s>>>(a, sink);
-    };
+    const unsigned grid = grid_for(l.nrows);
+    if (grid > sink.capacity) return false;
+    auto go = [&](auto kernel) { kernel<<<grid, 256, 0, s>>>(a, sink.partials); };
     if (l.sorted) {
         scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
     } else {
         scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
     }
     launched("k1_dot_kernel");
+    cg::dot_final_kernel<<<1, 1024, 0, s>>>(sink.partials, grid, sink.st, sink.dist);
+    launched("cg::dot_final_kernel");
     return true;
 }
 
