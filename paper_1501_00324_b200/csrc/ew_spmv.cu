@@ -110,7 +110,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
 // K1 / K1r / K1rs (warp_spmv.cpp:9-60): one thread per sorted row position.
 // SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
 template <bool SORTED, bool SCATTER, bool ROW_MAJOR>
-__global__ void __launch_bounds__(256) k1_kernel(K1Args a) {
+__global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= a.nrows || (a.done && *a.done)) return;
     const uint64_t pol = evict_first_policy();
