@@ -176,6 +176,40 @@ def test_device_buffers_and_streams(ew, R, F):
 
 BASELINES = ["csr_vector", "coo", "ell", "hyb"]
 
+# the reference's desk-scale stand-ins for the paper's 15 matrices
+# (bench/fetch.cpp:16-46); config 3 runs them at Table 2 sizes in bench.py
+REGISTRY = [
+    "powerlaw_rows:nrows=2048,alpha=1.4,maxrow=353,seed=11",
+    "powerlaw_rows:nrows=2048,alpha=0.8,maxrow=44,seed=12",
+    "uniform_band:n=4096,row_len=4",
+    "fem_tet_graph:n=2048,minrow=8,maxrow=81,seed=13",
+    "fem_tet_graph:n=1024,minrow=2,maxrow=78,seed=14",
+    "fem_tet_graph:n=1024,minrow=4,maxrow=145,seed=15",
+    "fem_tet_graph:n=2048,minrow=24,maxrow=102,seed=16",
+    "fem_tet_graph:n=1024,minrow=2,maxrow=81,seed=17",
+    "fem_tet_graph:n=1024,minrow=18,maxrow=204,seed=18",
+    "uniform_band:n=2048,row_len=39",
+    "powerlaw_rows:nrows=2000,alpha=2.0,maxrow=1000,seed=19",
+    "fem_tet_graph:n=2048,minrow=2,maxrow=180,seed=20",
+    "fem_tet_graph:n=3129,minrow=5,maxrow=21,seed=3",
+    "fem_tet_graph:n=4563,minrow=6,maxrow=22,seed=5",
+    "fem_tet_graph:n=28639,minrow=6,maxrow=24,seed=30",
+]
+
+
+@pytest.mark.parametrize("spec", REGISTRY)
+def test_paper_suite_standins_all_kernels(ew, F, spec):
+    """Every kernel id on the reference's stand-ins for the paper's suite,
+    bitwise against the compiled reference (K2 at three thresholds)."""
+    m = F.generate(spec)
+    x = F.random_vector(m.ncols, 99)
+    a = dev_csr(ew, m)
+    for kid in ["csr_ref", "csr_vector", "coo", "ell", "hyb", "k1", "k1r", "k1rs"]:
+        assert same(ew.Kernel(kid, a).apply(x), F.apply(kid, m, x)), kid
+    for t in (3, 16, 0):
+        for kid in ("k2", "k2r", "k2rs"):
+            assert same(ew.Kernel(kid, a, threshold=t).apply(x), F.apply(kid, m, x, threshold=t)), (kid, t)
+
 
 @pytest.mark.parametrize("case", range(0, 40, 2))
 def test_baseline_formats_match_reference(ew, F, case):
