@@ -608,6 +608,71 @@ def run_suite(args):
             "rows": rows}
 
 
+def run_alpha(args):
+    """the paper's break-even analysis (Table 5,
+    PAPER.md:598-626; analyze_alpha, bench.cpp:252-319) on the device.
+    t_base: baseline SpMV; t_kernel: reordered kernel in permuted space;
+    t_reorder: bulk_scatter = values-only refresh through the slot map,
+    host_loop = full device rebuild (sort + renumber + layout).
+    alpha = compute_alpha(t_reorder, t_kernel, t_base)."""
+    import torch
+
+    from paper_1501_00324_b200 import capi, load_ellwarp
+
+    ew_mod = load_ellwarp()
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+
+    def time_dev(fn, reps):
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return float(np.median(ts))
+
+    def time_host(fn, reps):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+        return float(np.median(ts))
+
+    rows = []
+    for name, n, kind, p in SUITE:
+        m = suite_matrix(ew_mod, kind, n, p)
+        ro = np.asarray(m.row_offsets, np.int64)
+        a = capi.Csr(m.nrows, m.ncols, ro, np.asarray(m.col_indices, np.int64), np.asarray(m.values))
+        x = torch.tensor(np.random.default_rng(1).uniform(0.1, 1.0, m.ncols), device="cuda")
+        y = torch.empty(m.nrows, dtype=torch.float64, device="cuda")
+        base = capi.Kernel("csr_ref", a)
+        t_base = time_dev(lambda: base.apply(x, y, stream=stream), args.alpha_reps)
+        for kid in ("k1rs", "k2rs"):
+            k = capi.Kernel(kid, a)
+            t_kernel = time_dev(lambda: k.apply_permuted(x, y, stream=stream), args.alpha_reps)
+            t_bulk = time_dev(lambda: k.refresh_values(a, stream=stream), args.alpha_reps)
+            t_rebuild = time_host(lambda: capi.Kernel(kid, a), max(3, args.alpha_reps // 3))
+            rows.append({"matrix": name, "nnz": a.nnz, "kernel": kid, "baseline": "csr_ref",
+                         "t_base_us": round(t_base * 1e6, 2), "t_kernel_us": round(t_kernel * 1e6, 2),
+                         "t_reorder_bulk_us": round(t_bulk * 1e6, 2), "t_reorder_rebuild_us": round(t_rebuild * 1e6, 1),
+                         "alpha_bulk": capi.compute_alpha(t_bulk, t_kernel, t_base),
+                         "alpha_rebuild": capi.compute_alpha(t_rebuild, t_kernel, t_base)})
+            log(f"[alpha] {name} {kid}: base {t_base*1e6:.1f}us kernel {t_kernel*1e6:.1f}us "
+                f"bulk {t_bulk*1e6:.1f}us rebuild {t_rebuild*1e3:.2f}ms -> alpha {rows[-1]['alpha_bulk']} / "
+                f"{rows[-1]['alpha_rebuild']}")
+            del k
+        del a, base
+        torch.cuda.empty_cache()
+    return {"metric": "alpha: SpMV calls to amortise the reorder (None = never)", "workload":
+            "config 3 structures, reordered kernel vs csr_ref, device timings (warm)", "rows": rows}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
@@ -644,7 +709,8 @@ def main():
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["spmv", "cg", "suite"], default="spmv")
+    p.add_argument("--workload", choices=["spmv", "cg", "suite", "alpha"], default="spmv")
+    p.add_argument("--alpha-reps", type=int, default=9)
     p.add_argument("--suite-iters", type=int, default=10)
     p.add_argument("--config", default=None)
     p.add_argument("--kernel", default=None)
@@ -671,9 +737,9 @@ def main():
             print(json.dumps(out), flush=True)
         return
     rank, world, local = dist_init(args.gpus)
-    if args.workload == "suite":
+    if args.workload in ("suite", "alpha"):
         if rank == 0:
-            print(json.dumps(run_suite(args)), flush=True)
+            print(json.dumps(run_suite(args) if args.workload == "suite" else run_alpha(args)), flush=True)
         return
     out = run_spmv(args, rank, world, local) if args.workload == "spmv" else run_cg(args, rank, world, local)
     if rank == 0:

@@ -478,8 +478,9 @@ ew_status ew_kernel_refresh_values(ew_kernel k, ew_csr m, void* stream) {
             return;
         }
         if (d.reordered)
-            throw ew::Error(EW_UNSUPPORTED, "values-only refresh of r/rs kernels is not implemented yet");
-        ew::layout_refresh_values(*d.layout, *m->d, s);
+            ew::layout_refresh_values_reordered(*d.layout, *m->d, d.entry_dst.get(), s);
+        else
+            ew::layout_refresh_values(*d.layout, *m->d, s);
     });
 }
 

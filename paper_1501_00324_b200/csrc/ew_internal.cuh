@@ -160,6 +160,7 @@ struct KernelData {
     std::shared_ptr<CsrData> csr;        // csr_ref, and the arrays of csr_vector / coo
     std::shared_ptr<LayoutData> layout;  // k1* / k2*
     std::shared_ptr<FormatData> format;  // csr_vector / coo / ell / hyb
+    DevBuf<int64_t> entry_dst;           // r / rs: original entry -> reordered entry (refresh)
 };
 
 std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
@@ -181,8 +182,11 @@ void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
 // make_reordered_r / make_reordered_rs (reorder.cpp:8-43): renumber columns
 // by a permutation (fwd_in, host, nullable = sort_rows_desc) and/or sort each
 // row's (column, value) pairs by column.
+// dst_of (nullable) receives, per input entry, its index in the output.
 std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool renumber,
-                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s);
+                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s,
+                                 DevBuf<int64_t>* dst_of = nullptr);
+void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s);
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s);

@@ -28,7 +28,7 @@ std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, 
         std::shared_ptr<CsrData> op;
         if (reordered) {
             require(src.nrows == src.ncols, "kernel '" + sid + "' requires a square matrix");
-            op = reorder(src, nullptr, true, sid.size() == 4, nullptr, s);
+            op = reorder(src, nullptr, true, sid.size() == 4, nullptr, s, &k->entry_dst);
         }
         k->reordered = reordered;
         k->layout = build_layout(reordered ? *op : src, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false, s);

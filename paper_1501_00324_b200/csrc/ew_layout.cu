@@ -226,7 +226,7 @@ __global__ void renumber_kernel(const int32_t* __restrict__ ci, const int32_t* _
 // destination is its rank among the row's (distinct) renumbered columns.
 __global__ void row_rank_sort_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ c_in,
                                      const double* __restrict__ v_in, int32_t* __restrict__ c_out,
-                                     double* __restrict__ v_out, int64_t nrows) {
+                                     double* __restrict__ v_out, int64_t* __restrict__ dst_of, int64_t nrows) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
@@ -239,8 +239,23 @@ __global__ void row_rank_sort_kernel(const int64_t* __restrict__ ro, const int32
             for (int64_t q = lo; q < hi; ++q) rank += (c_in[q] < c || (c_in[q] == c && q < k)) ? 1 : 0;
             c_out[lo + rank] = c;
             v_out[lo + rank] = v_in[k];
+            if (dst_of) dst_of[k] = lo + rank;  // where entry k of the input went
         }
     }
+}
+
+__global__ void iota_kernel(int64_t* __restrict__ out, int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = k;
+}
+
+// Values-only refresh of a layout built on a reordered operand: entry k of
+// the ORIGINAL matrix sits at reordered index dst_of[k], whose slot is
+// slot_map[dst_of[k]] (the rows keep their offsets under r / rs).
+__global__ void refresh_reordered_kernel(const int64_t* __restrict__ slot_map, const int64_t* __restrict__ dst_of,
+                                         const double* __restrict__ v, double* __restrict__ out, int64_t nnz) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < nnz) out[slot_map[dst_of[k]]] = v[k];
 }
 
 unsigned fill_grid(int64_t nwarps) {
@@ -331,8 +346,9 @@ void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
 }
 
 std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool renumber,
-                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s) {
+                                 bool sort_within_rows, int32_t* fwd_out, cudaStream_t s, DevBuf<int64_t>* dst_of) {
     const int64_t n = m.nrows, nnz = m.nnz;
+    if (dst_of) dst_of->alloc(nnz);
     Scratch<int32_t> fwd(renumber ? n : 0, s), inv(renumber ? n : 0, s), slen(renumber ? n : 0, s);
     if (renumber) {
         require(m.nrows == m.ncols, "make_reordered_r: matrix must be square");
@@ -375,12 +391,16 @@ std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool r
             EW_CUDA_CHECK(cudaMemcpyAsync(cdst, m.ci.get(), nnz * 4, cudaMemcpyDeviceToDevice, s));
         }
         if (sort_within_rows) {
-            row_rank_sort_kernel<<<fill_grid(n), 256, 0, s>>>(m.ro.get(), tmp.get(), m.v.get(),
-                                                              out->ci.get(), out->v.get(), n);
+            row_rank_sort_kernel<<<fill_grid(n), 256, 0, s>>>(m.ro.get(), tmp.get(), m.v.get(), out->ci.get(),
+                                                              out->v.get(), dst_of ? dst_of->get() : nullptr, n);
             launched("row_rank_sort_kernel");
         } else {
             EW_CUDA_CHECK(cudaMemcpyAsync(out->v.get(), m.v.get(), nnz * sizeof(double),
                                           cudaMemcpyDeviceToDevice, s));
+            if (dst_of) {
+                iota_kernel<<<grid_for(nnz), kBlock, 0, s>>>(dst_of->get(), nnz);
+                launched("iota_kernel");
+            }
         }
     }
     if (fwd_out && renumber && n)
@@ -530,6 +550,16 @@ void layout_build_slot_map(LayoutData& l, const CsrData& m, cudaStream_t s) {
         slot_map_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(mapper_of(l, m), l.slot_map.get());
         launched("slot_map_kernel");
     }
+}
+
+void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s) {
+    // the r / rs operand keeps m's row offsets, so m itself serves to map
+    // reordered entries to slots; dst_of takes original entries there
+    layout_build_slot_map(l, m, s);
+    if (!m.nnz) return;
+    refresh_reordered_kernel<<<grid_for(m.nnz), kBlock, 0, s>>>(l.slot_map.get(), dst_of, m.v.get(), l.values.get(),
+                                                                m.nnz);
+    launched("refresh_reordered_kernel");
 }
 
 void layout_refresh_values(LayoutData& l, const CsrData& m, cudaStream_t s) {

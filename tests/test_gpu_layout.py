@@ -121,6 +121,30 @@ def test_import_round_trip_and_refresh(ew, R, F):
         ew.Layout.import_arrays("k1", 32, 3, 3, 1, [1.0], [0], [0], [5], [3], [0, 1, 1], [1, 0, 0])
 
 
+@pytest.mark.parametrize("kid", ["csr_ref", "k1", "k2", "k1r", "k1rs", "k2r", "k2rs", "csr_vector", "coo"])
+def test_kernel_values_refresh(ew, F, kid):
+    """Values-only refresh of a prepared kernel (the paper's reorder once per
+    Newton iteration): same structure, new values -> the
+    refreshed kernel equals one prepared from scratch, bit for bit."""
+    from tests.gpu_helpers import same
+
+    m = F.fem_tet_graph(1200, 5, 21, 9)
+    x = F.random_vector(m.ncols, 4)
+    a = dev_csr(ew, m)
+    k = ew.Kernel(kid, a, threshold=5)
+    v2 = np.sin(np.arange(m.nnz)) + 2.0
+    b = ew.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, v2)
+    k.refresh_values(b)
+    fresh = ew.Kernel(kid, b, threshold=5)
+    assert same(k.apply(x), fresh.apply(x)), kid
+    if k.has_perm:
+        assert same(k.apply_permuted(x), fresh.apply_permuted(x))
+    # the prepared kernel owns its matrix: updating the source handle later
+    # does not reach it (kernels.cpp:65-68 copies the matrix)
+    b.update_values(v2 * 3.0)
+    assert same(k.apply(x), fresh.apply(x))
+
+
 def test_kernel_stored_slots(ew, R, F):
     """PreparedKernel::stored_slots (kernels.cpp:63, 104, 112) and padding claims
     (acceptance.cpp criterion 3): sorted K1 pads less than unsorted."""
