@@ -129,11 +129,12 @@ struct LayoutData {
     DevBuf<int64_t> warp_offset;
     DevBuf<int32_t> maxrows, rows_in_warp, reduction, rows_offset_warp;
     DevBuf<int32_t> fwd, inv, slen;
-    DevBuf<int64_t> slot_map;  // lazily built value_slot_map (values-only refresh)
+    DevBuf<int64_t> slot_map;  // lazily built value_slot_map (export)
+    DevBuf<int64_t> src_map;   // lazily built per-slot source entry (values-only refresh)
     size_t device_bytes() const {
         return values.bytes() + cols.bytes() + warp_offset.bytes() + maxrows.bytes() +
                rows_in_warp.bytes() + reduction.bytes() + rows_offset_warp.bytes() + fwd.bytes() +
-               inv.bytes() + slen.bytes() + slot_map.bytes();
+               inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes();
     }
 };
 

@@ -209,10 +209,41 @@ __global__ void slot_map_kernel(SlotMapper M, int64_t* __restrict__ map) {
     }
 }
 
-__global__ void refresh_kernel(const int64_t* __restrict__ map, const double* __restrict__ v,
-                               double* __restrict__ out, int64_t nnz) {
+// Per-slot source entry (-1 for padding and alignment gaps): the inverse of
+// value_slot_map, so the values-only refresh is a gather with coalesced
+// writes instead of a scatter through the slot map. orig_of (nullable) maps
+// the layout's operand entries (an r / rs matrix) back to the original's.
+__global__ void src_map_kernel(SlotMapper M, const int64_t* __restrict__ orig_of, int64_t* __restrict__ src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = gw; w < M.nwarps; w += nhw) {
+        const int64_t off = M.woff[w];
+        const int64_t end = w + 1 < M.nwarps ? M.woff[w + 1] : M.nslots;
+        const int32_t mx = M.maxrows[w];
+        const int32_t red = M.reduction ? M.reduction[w] : 1;
+        const int64_t first = M.rows_offset_warp ? M.rows_offset_warp[w] : (w << M.ws_log2);
+        const int32_t nr = M.rows_in_warp[w];
+        const int64_t count = int64_t(mx) * M.ws;
+        for (int64_t local = lane; local < end - off; local += 32) {
+            int64_t k = local < count ? M.source(w, local, mx, red, first, nr) : -1;
+            if (k >= 0 && orig_of) k = orig_of[k];
+            src[off + local] = k;
+        }
+    }
+}
+
+__global__ void refresh_gather_kernel(const int64_t* __restrict__ src, const double* __restrict__ v,
+                                      double* __restrict__ out, int64_t nslots) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    const int64_t k = src[s];
+    if (k >= 0) out[s] = v[k];  // padding slots keep their 0.0
+}
+
+__global__ void invert_kernel(const int64_t* __restrict__ dst_of, int64_t* __restrict__ orig_of, int64_t n) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < nnz) out[map[k]] = v[k];
+    if (k < n) orig_of[dst_of[k]] = k;
 }
 
 // make_reordered_r (reorder.cpp:8-17): c -> inverse[c]
@@ -249,14 +280,6 @@ __global__ void iota_kernel(int64_t* __restrict__ out, int64_t n) {
     if (k < n) out[k] = k;
 }
 
-// Values-only refresh of a layout built on a reordered operand: entry k of
-// the ORIGINAL matrix sits at reordered index dst_of[k], whose slot is
-// slot_map[dst_of[k]] (the rows keep their offsets under r / rs).
-__global__ void refresh_reordered_kernel(const int64_t* __restrict__ slot_map, const int64_t* __restrict__ dst_of,
-                                         const double* __restrict__ v, double* __restrict__ out, int64_t nnz) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < nnz) out[slot_map[dst_of[k]]] = v[k];
-}
 
 unsigned fill_grid(int64_t nwarps) {
     // 8 hardware warps per CTA, enough CTAs to cover every SM several times.
@@ -552,21 +575,37 @@ void layout_build_slot_map(LayoutData& l, const CsrData& m, cudaStream_t s) {
     }
 }
 
+namespace {
+void ensure_src_map(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s) {
+    require(m.nrows == l.nrows && m.nnz == l.nnz, "refresh: matrix does not match the layout");
+    if (l.src_map.size() == size_t(l.nslots)) return;
+    // the r / rs operand keeps m's row offsets, so m maps the operand's
+    // entries to slots; orig_of = dst_of^-1 takes them back to m's entries
+    Scratch<int64_t> orig_of(dst_of ? m.nnz : 0, s);
+    if (dst_of && m.nnz) {
+        invert_kernel<<<grid_for(m.nnz), kBlock, 0, s>>>(dst_of, orig_of.get(), m.nnz);
+        launched("invert_kernel");
+    }
+    l.src_map.alloc(l.nslots);
+    if (l.nwarps) {
+        src_map_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(mapper_of(l, m), dst_of ? orig_of.get() : nullptr,
+                                                           l.src_map.get());
+        launched("src_map_kernel");
+    }
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));  // orig_of is freed on return
+}
+}  // namespace
+
 void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s) {
-    // the r / rs operand keeps m's row offsets, so m itself serves to map
-    // reordered entries to slots; dst_of takes original entries there
-    layout_build_slot_map(l, m, s);
-    if (!m.nnz) return;
-    refresh_reordered_kernel<<<grid_for(m.nnz), kBlock, 0, s>>>(l.slot_map.get(), dst_of, m.v.get(), l.values.get(),
-                                                                m.nnz);
-    launched("refresh_reordered_kernel");
+    ensure_src_map(l, m, dst_of, s);
+    if (!l.nslots) return;
+    refresh_gather_kernel<<<grid_for(l.nslots), kBlock, 0, s>>>(l.src_map.get(), m.v.get(), l.values.get(),
+                                                                l.nslots);
+    launched("refresh_gather_kernel");
 }
 
 void layout_refresh_values(LayoutData& l, const CsrData& m, cudaStream_t s) {
-    layout_build_slot_map(l, m, s);
-    if (!m.nnz) return;
-    refresh_kernel<<<grid_for(m.nnz), kBlock, 0, s>>>(l.slot_map.get(), m.v.get(), l.values.get(), m.nnz);
-    launched("refresh_kernel");
+    layout_refresh_values_reordered(l, m, nullptr, s);
 }
 
 std::shared_ptr<LayoutData> import_layout(const ew_layout_desc& d, cudaStream_t s) {
