@@ -90,6 +90,27 @@ def test_smoke_construct_and_stats(ew_mod, ew):
 
 
 @pytest.mark.gpu
+def test_smoke_matrix_market_roundtrip(ew_mod, ew, tmp_path):
+    # test_smoke.py:23-28: symmetric storage expands, bogus header raises
+    text = "%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n2 1 5.0\n2 2 1.0\n"
+    m = ew_mod.parse_matrix_market(text)
+    assert m.nnz() == 3 and m.col_indices == [1, 0, 1] and m.values == [5.0, 5.0, 1.0]
+    with pytest.raises(Exception):
+        ew_mod.parse_matrix_market("%%bogus\n")
+    with pytest.raises(Exception):
+        ew_mod.parse_matrix_market("%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n")
+    import gzip
+
+    body = "%%MatrixMarket matrix coordinate pattern general\n% comment\n3 3 2\n1 3\n3 1\n"
+    (tmp_path / "p.mtx").write_text(body)
+    with gzip.open(tmp_path / "p.mtx.gz", "wt") as f:
+        f.write(body)
+    for name in ("p.mtx", "p.mtx.gz"):
+        p = ew_mod.read_matrix_market(str(tmp_path / name))
+        assert p.nrows == 3 and p.row_offsets == [0, 1, 1, 2] and p.col_indices == [2, 0] and p.values == [1.0, 1.0]
+
+
+@pytest.mark.gpu
 def test_smoke_device_kernels_match_reference(ew_mod, ew):
     m = ew_mod.fem_tet_graph(500, 5, 21, seed=7)
     x = [0.1 + 0.001 * i for i in range(m.ncols)]
