@@ -316,6 +316,30 @@ ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, v
 ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const ew_cg_config* cfg,
                            ew_mem_kind mem, double* x, double* history, ew_cg_result* result,
                            void* stream);
+/* ---- FEM assembly as K1 row sums (fem/assembly.cpp:38-159, SURVEY.md
+ * §8(f) #3) ---------------------------------------------------------------
+ * build_assembly_map on the device: the node-adjacency pattern of the
+ * tetrahedra (elements: int64[nelements * 4], host), one contribution row per
+ * pattern entry / per node in element-major order, packed into K1 layouts. */
+typedef struct ew_assembly_t* ew_assembly;
+ew_status ew_assembly_create(int64_t nelements, const int64_t* elements, int64_t nnodes,
+                             const ew_warp_config* cfg, ew_assembly* out);
+ew_status ew_assembly_destroy(ew_assembly a);
+/* The tangent pattern (host; arrays nullable, call with NULL to size). */
+ew_status ew_assembly_pattern(ew_assembly a, int64_t* nnz, int64_t* row_offsets,
+                              int64_t* col_indices);
+/* assemble_spmv (fem/assembly.cpp:140-159): ke = element tangents
+ * [nelements][4][4], re = element residuals [nelements][4]; outputs the
+ * tangent values in pattern order and the residual (either may be NULL).
+ * Bit-identical to the reference's scatter + row sum. */
+ew_status ew_assembly_run(ew_assembly a, const double* ke, const double* re,
+                          double* tangent_values, double* residual, ew_mem_kind mem,
+                          void* stream);
+/* The same, but the tangent lands directly in the slots of kernel k (an
+ * ELL-WARP kernel prepared on the pattern): no values refresh before the
+ * next SpMV / CG. */
+ew_status ew_assembly_run_into(ew_assembly a, const double* ke, const double* re, ew_kernel k,
+                               double* residual, ew_mem_kind mem, void* stream);
 /* compute_alpha (cg.cpp:121-132); *finite = 0 means infinity. */
 ew_status ew_compute_alpha(double t_reorder, double t_kernel, double t_base, int64_t* alpha,
                            int32_t* finite);

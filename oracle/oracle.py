@@ -519,6 +519,26 @@ class Reference:
         self._check(self.lib.refw_compute_alpha(tr, tk, tb, C.byref(a), C.byref(f)))
         return int(a.value) if f.value else None
 
+    # FEM assembly (fem/mesh.cpp, fem/assembly.cpp)
+    def box_elements(self, nx, ny, nz):
+        self.lib.refw_box_elements.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+        b = self._bag(self.lib.refw_box_elements, nx, ny, nz)
+        try:
+            return self._bi(b, 0).reshape(-1, 4), int(self.lib.refw_bag_scalar(b, 0))
+        finally:
+            self.lib.refw_bag_free(b)
+
+    def box_assemble(self, nx, ny, nz, ke, re, warp_size=32):
+        """assemble_spmv on box_mesh: (pattern ro, pattern ci, tangent, residual)."""
+        self.lib.refw_box_assemble.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, _f64p, _f64p, C.c_void_p]
+        ke = np.ascontiguousarray(ke, np.float64)
+        re = np.ascontiguousarray(re, np.float64)
+        b = self._bag(self.lib.refw_box_assemble, nx, ny, nz, warp_size, _fp(ke), _fp(re))
+        try:
+            return self._bi(b, 0), self._bi(b, 1), self._bd(b, 0), self._bd(b, 1)
+        finally:
+            self.lib.refw_bag_free(b)
+
 
 def reference_available():
     return os.path.exists(REFERENCE_SO)

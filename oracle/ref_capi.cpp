@@ -15,6 +15,8 @@
 #include <memory>
 
 #include "ellwarp/cg.hpp"
+#include "ellwarp/fem/assembly.hpp"
+#include "ellwarp/fem/mesh.hpp"
 #include "ellwarp/kernels.hpp"
 #include "ellwarp/synth.hpp"
 #include "test_support.hpp"  // the reference's own test corpus (random_case, random_vector)
@@ -312,6 +314,44 @@ int refw_cg(const char* id, int64_t nrows, int64_t ncols, const int64_t* ro, con
         bag->scalars[1] = res.converged ? 1 : 0;
         bag->scalars[2] = res.spmv_calls;
         *out = bag;
+    });
+}
+
+// fem::box_mesh connectivity (fem/mesh.cpp:33-71): i[0] = elements (ne x 4),
+// scalars {nnodes, nelements}
+int refw_box_elements(int64_t nx, int64_t ny, int64_t nz, Bag** out) {
+    return guard([&] {
+        const auto mesh = fem::box_mesh(nx, ny, nz);
+        auto* b = new Bag;
+        std::vector<int64_t> e;
+        e.reserve(mesh.elements.size() * 4);
+        for (const auto& t : mesh.elements) e.insert(e.end(), t.begin(), t.end());
+        b->i = {e};
+        b->scalars[0] = mesh.nnodes();
+        b->scalars[1] = mesh.nelements();
+        *out = b;
+    });
+}
+
+// assemble_spmv (fem/assembly.cpp:140-159) of given element outputs on
+// box_mesh(nx, ny, nz): i[0] = pattern row_offsets, i[1] = pattern columns,
+// d[0] = tangent values, d[1] = residual
+int refw_box_assemble(int64_t nx, int64_t ny, int64_t nz, int ws, const double* ke, const double* re, Bag** out) {
+    return guard([&] {
+        const auto mesh = fem::box_mesh(nx, ny, nz);
+        const auto map = fem::build_assembly_map(mesh, make_cfg(ws, 128, 1));
+        std::vector<fem::ElementOutput> outs(mesh.nelements());
+        for (int64_t e = 0; e < mesh.nelements(); ++e) {
+            for (int i = 0; i < 4; ++i) {
+                outs[e].Re[i] = re[4 * e + i];
+                for (int j = 0; j < 4; ++j) outs[e].Ke[i][j] = ke[16 * e + 4 * i + j];
+            }
+        }
+        const auto sys = fem::assemble_spmv(map, outs);
+        auto* b = new Bag;
+        b->i = {map.pattern.row_offsets, map.pattern.col_indices};
+        b->d = {sys.tangent_values, sys.residual};
+        *out = b;
     });
 }
 

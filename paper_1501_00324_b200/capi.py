@@ -148,6 +148,11 @@ _SIGS = {
     "ew_cg_solve_operator": (C.c_int, [OPERATOR_FN, _vp, C.c_int, _vp, _vp, C.c_int64, C.POINTER(CgConfig),
                                        C.c_int, _vp, _vp, C.POINTER(CgResultC), _vp]),
     "ew_compute_alpha": (C.c_int, [C.c_double, C.c_double, C.c_double, _i64p, C.POINTER(C.c_int32)]),
+    "ew_assembly_create": (C.c_int, [C.c_int64, _vp, C.c_int64, C.POINTER(WarpConfig), C.POINTER(_vp)]),
+    "ew_assembly_destroy": (C.c_int, [_vp]),
+    "ew_assembly_pattern": (C.c_int, [_vp, _i64p, _vp, _vp]),
+    "ew_assembly_run": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "ew_assembly_run_into": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
     "ew_partition_rows": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp]),
     "ew_nccl_unique_id": (C.c_int, [_vp]),
     "ew_dist_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, _vp, C.c_int32,
@@ -574,6 +579,49 @@ def cg_solve_operator(op, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=Tr
                                      EW_MEM_HOST, _ptr(x), _ptr(hist), C.byref(res), None))
     return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
                     int(res.spmv_calls))
+
+
+class Assembly:
+    """Race-free FEM assembly as K1 row sums (ew_assembly)."""
+
+    def __init__(self, elements, nnodes, warp_size=32):
+        e = _host(elements, np.int64).reshape(-1)
+        cfg = WarpConfig.make(warp_size)
+        h = C.c_void_p()
+        check(lib().ew_assembly_create(e.size // 4, _ptr(e), int(nnodes), C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.nelements = e.size // 4
+        self.nnodes = int(nnodes)
+        nnz = C.c_int64()
+        check(lib().ew_assembly_pattern(h, C.byref(nnz), None, None))
+        self.nnz = nnz.value
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.ew_assembly_destroy(h)
+            self.h = None
+
+    def pattern(self):
+        ro = np.empty(self.nnodes + 1, np.int64)
+        ci = np.empty(self.nnz, np.int64)
+        check(lib().ew_assembly_pattern(self.h, None, _ptr(ro), _ptr(ci)))
+        return ro, ci
+
+    def run(self, ke, re):
+        ke = _host(ke, np.float64)
+        re = _host(re, np.float64)
+        t = np.empty(self.nnz, np.float64)
+        r = np.empty(self.nnodes, np.float64)
+        check(lib().ew_assembly_run(self.h, _ptr(ke), _ptr(re), _ptr(t), _ptr(r), EW_MEM_HOST, None))
+        return t, r
+
+    def run_into(self, ke, re, kernel):
+        ke = _host(ke, np.float64)
+        re = _host(re, np.float64)
+        r = np.empty(self.nnodes, np.float64)
+        check(lib().ew_assembly_run_into(self.h, _ptr(ke), _ptr(re), kernel.h, _ptr(r), EW_MEM_HOST, None))
+        return r
 
 
 def partition_rows(row_offsets, nparts):

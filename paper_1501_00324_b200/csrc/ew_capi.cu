@@ -18,6 +18,9 @@ struct ew_kernel_t {
 struct ew_dist_t {
     std::shared_ptr<ew::DistData> d;
 };
+struct ew_assembly_t {
+    std::shared_ptr<ew::AssemblyData> d;
+};
 
 namespace {
 
@@ -712,6 +715,76 @@ ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
         *result = o.res;
         if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+    });
+}
+
+ew_status ew_assembly_create(int64_t nelements, const int64_t* elements, int64_t nnodes, const ew_warp_config* cfg,
+                             ew_assembly* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && (elements != nullptr || nelements == 0), "null argument");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        *out = new ew_assembly_t{ew::assembly_create(nelements, elements, nnodes, c, nullptr)};
+    });
+}
+
+ew_status ew_assembly_destroy(ew_assembly a) {
+    return guarded([&] { delete a; });
+}
+
+ew_status ew_assembly_pattern(ew_assembly a, int64_t* nnz, int64_t* row_offsets, int64_t* col_indices) {
+    return guarded([&] {
+        check_handle(a, "assembly");
+        if (nnz) *nnz = ew::assembly_nnz(*a->d);
+        ew::assembly_pattern(*a->d, row_offsets, col_indices);
+    });
+}
+
+ew_status ew_assembly_run(ew_assembly a, const double* ke, const double* re, double* tangent_values, double* residual,
+                          ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(a, "assembly");
+        const auto& A = *a->d;
+        const cudaStream_t s = ew::as_stream(stream);
+        const int64_t ne = A.nelements, nnz = ew::assembly_nnz(A), nn = A.nnodes;
+        if (mem == EW_MEM_DEVICE) {
+            ew::assembly_run(A, ke, re, tangent_values, nullptr, residual, s);
+            EW_CUDA_CHECK(cudaGetLastError());
+            return;
+        }
+        ew::Scratch<double> dke(ke ? 16 * ne : 0, s), dre(re ? 4 * ne : 0, s), dt(tangent_values ? nnz : 0, s),
+            dr(residual ? nn : 0, s);
+        if (ke && ne) EW_CUDA_CHECK(cudaMemcpyAsync(dke.get(), ke, 16 * ne * 8, cudaMemcpyHostToDevice, s));
+        if (re && ne) EW_CUDA_CHECK(cudaMemcpyAsync(dre.get(), re, 4 * ne * 8, cudaMemcpyHostToDevice, s));
+        ew::assembly_run(A, dke.get(), dre.get(), tangent_values ? dt.get() : nullptr, nullptr,
+                         residual ? dr.get() : nullptr, s);
+        if (tangent_values && nnz)
+            EW_CUDA_CHECK(cudaMemcpyAsync(tangent_values, dt.get(), nnz * 8, cudaMemcpyDeviceToHost, s));
+        if (residual && nn) EW_CUDA_CHECK(cudaMemcpyAsync(residual, dr.get(), nn * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+ew_status ew_assembly_run_into(ew_assembly a, const double* ke, const double* re, ew_kernel k, double* residual,
+                               ew_mem_kind mem, void* stream) {
+    return guarded([&] {
+        check_handle(a, "assembly");
+        check_handle(k, "kernel");
+        const auto& A = *a->d;
+        const cudaStream_t s = ew::as_stream(stream);
+        const int64_t ne = A.nelements, nn = A.nnodes;
+        if (mem == EW_MEM_DEVICE) {
+            ew::assembly_run_into(A, ke, re, *k->d, residual, s);
+            EW_CUDA_CHECK(cudaGetLastError());
+            return;
+        }
+        ew::Scratch<double> dke(16 * ne, s), dre(4 * ne, s), dr(residual ? nn : 0, s);
+        if (ne) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(dke.get(), ke, 16 * ne * 8, cudaMemcpyHostToDevice, s));
+            EW_CUDA_CHECK(cudaMemcpyAsync(dre.get(), re, 4 * ne * 8, cudaMemcpyHostToDevice, s));
+        }
+        ew::assembly_run_into(A, dke.get(), dre.get(), *k->d, residual ? dr.get() : nullptr, s);
+        if (residual && nn) EW_CUDA_CHECK(cudaMemcpyAsync(residual, dr.get(), nn * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
 

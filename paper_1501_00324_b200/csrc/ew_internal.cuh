@@ -188,6 +188,25 @@ std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool r
                                  bool sort_within_rows, int32_t* fwd_out, cudaStream_t s,
                                  DevBuf<int64_t>* dst_of = nullptr);
 void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s);
+// out[slot] = source entry of m for every slot of l (-1 for padding), mapped
+// through orig_of when given.
+void layout_src_map(const LayoutData& l, const CsrData& m, const int64_t* orig_of, int64_t* out, cudaStream_t s);
+
+// ---- FEM assembly as K1 row sums (ew_assembly.cu) ----
+struct AssemblyData {
+    int64_t nelements = 0, nnodes = 0, nnz = 0;
+    CsrData pattern;  // global tangent sparsity (values zero), diagonal included
+    std::shared_ptr<LayoutData> tangent, residual;  // K1 layouts over contribution rows
+    DevBuf<int64_t> tangent_src, residual_src;      // per slot: element-output index or -1
+};
+std::shared_ptr<AssemblyData> assembly_create(int64_t ne, const int64_t* elements_host, int64_t nnodes,
+                                              const ew_warp_config& cfg, cudaStream_t s);
+void assembly_pattern(const AssemblyData& A, int64_t* ro, int64_t* ci);
+int64_t assembly_nnz(const AssemblyData& A);
+void assembly_run(const AssemblyData& A, const double* ke, const double* re, double* tangent, const int64_t* dest,
+                  double* residual, cudaStream_t s);
+void assembly_run_into(const AssemblyData& A, const double* ke, const double* re, KernelData& k, double* residual,
+                       cudaStream_t s);
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s);

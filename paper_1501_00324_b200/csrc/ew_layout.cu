@@ -596,6 +596,12 @@ void ensure_src_map(LayoutData& l, const CsrData& m, const int64_t* dst_of, cuda
 }
 }  // namespace
 
+void layout_src_map(const LayoutData& l, const CsrData& m, const int64_t* orig_of, int64_t* out, cudaStream_t s) {
+    if (!l.nwarps) return;
+    src_map_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(mapper_of(l, m), orig_of, out);
+    launched("src_map_kernel");
+}
+
 void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s) {
     ensure_src_map(l, m, dst_of, s);
     if (!l.nslots) return;
