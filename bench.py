@@ -56,6 +56,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(key):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[key]["traffic_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def build_matrix(cfg_key, scale=1.0):
     from paper_1501_00324_b200 import workloads as W
 
@@ -330,7 +340,9 @@ def run_spmv(args, rank, world, local):
         "effective_pct_of_hbm": round(100 * value / world / hbm, 2),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
+                     "frac": round(achieved / hbm, 4) if achieved else None,
+                     "traffic": ncu_traffic(f"{args.config}/{args.kernel}") if args.scale == 1.0 else None,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
                      "kernel": "k1_kernel" if args.kernel.startswith("k1") else "k2_kernel",
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
@@ -438,7 +450,16 @@ def run_cg_dist(args, rank, world, local):
     nnz_all, n_all = sum_over_ranks([float(nnz), float(nloc)], world)
     b_it = 12 * nnz_all + 104 * n_all + (12 * nnz_all + 24 * n_all) / 50
     per_gpu = b_it / world * it_s / 1e9
+    # end to end: host b / diag in, solution + history out, every rank
+    bh, dh = b.cpu().numpy(), diag
+    barrier(world)
+    t = time.perf_counter()
+    d.cg_solve(bh, dh, tol=1e-300, max_iterations=iters)
+    e2e_s = max_over_ranks(time.perf_counter() - t, world)
     return {
+        "e2e": {"value": round(iters / e2e_s, 2), "unit": "it/s", "h2d_bytes_per_step": 16 * nloc,
+                "d2h_bytes_per_step": 8 * nloc + 8 * (iters + 1),
+                "path": "ew_dist_cg_solve(EW_MEM_HOST) per rank"},
         "metric": "CG iterations/s", "value": round(it_s, 2), "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -499,6 +520,15 @@ def run_cg(args, rank, world, local):
                      "traffic": None, "algorithmic_bytes_per_iteration": b_it},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    # end to end through ew_cg_solve[_permuted] with host b / diag / x
+    bh = np.ascontiguousarray(b)
+    t = time.perf_counter()
+    for _ in range(max(1, min(args.steps, 2))):
+        k.cg_solve(bh, diag, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+    e2e_s = (time.perf_counter() - t) / max(1, min(args.steps, 2))
+    out["e2e"] = {"value": round(iters / e2e_s, 2), "unit": "it/s", "h2d_bytes_per_step": 16 * n,
+                  "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
+                  "path": "ew_cg_solve_permuted(EW_MEM_HOST): b, diag in, solution + history out"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, its, dt = reference_cg_rate(n, nc, ro, ci, v, iters=max(2, args.cpu_cg_iters))
         out["cpu_baseline"] = {"value": round(rate, 3), "unit": "it/s", "cores": 1, "kind": "reference",
