@@ -395,7 +395,19 @@ def run_spmv_dist(args, rank, world, local):
     eff, alg, nnz_all = sum_over_ranks([20.0 * nnz, 12.0 * nnz + 16.0 * nloc, float(nnz)], world)
     value = eff / (ms * 1e-3) / 1e9
     per_gpu_alg = alg / world / (ms * 1e-3) / 1e9
+    # end to end: host x slice in, host y slice out on every rank
+    xh = x.cpu().numpy()
+    k_e2e = max(3, min(args.steps, 30))
+    d.spmv(xh)
+    barrier(world)
+    t = time.perf_counter()
+    for _ in range(k_e2e):
+        d.spmv(xh)
+    e2e_ms = max_over_ranks((time.perf_counter() - t) * 1e3 / k_e2e, world)
     return {
+        "e2e": {"value": round(eff / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nloc,
+                "d2h_bytes_per_step": 8 * nloc, "ms_per_step": round(e2e_ms, 4),
+                "path": "ew_dist_spmv(EW_MEM_HOST) per rank"},
         "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)", "value": round(value, 2), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
