@@ -267,7 +267,7 @@ def run_spmv(args, rank, world, local):
     nnz = int(ro[-1])
     t = time.time()
     a = capi.Csr(n, nc, ro, ci, v)
-    k = capi.Kernel(args.kernel, a, threshold=args.threshold)
+    k = capi.Kernel(args.kernel, a, threshold=args.threshold, row_order=args.row_order)
     torch.cuda.synchronize()
     t_prepare = time.time() - t
     log(f"[bench] rank {rank}: upload+validate+prepare({args.kernel}) {t_prepare:.2f}s, "
@@ -497,7 +497,11 @@ def run_cg(args, rank, world, local):
     n, nc, ro, ci, v = build_matrix(args.config, args.scale)
     nnz = int(ro[-1])
     a = capi.Csr(n, nc, ro, ci, v)
-    k = capi.Kernel(args.kernel, a, threshold=args.threshold)
+    t = time.time()
+    k = capi.Kernel(args.kernel, a, threshold=args.threshold, row_order=args.row_order)
+    torch.cuda.synchronize()
+    t_prepare = time.time() - t
+    log(f"[bench] prepare({args.kernel}, row_order={args.row_order}) {t_prepare:.2f}s")
     diag = a.extract_diagonal()
     b = a.spmv(np.ones(nc))  # b = A * 1 (ellwarp_cli.cpp:192-195)
     bd = torch.tensor(b, device="cuda")
@@ -526,7 +530,8 @@ def run_cg(args, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
-                   "iterations_per_step": iters, "nrows": n, "nnz": nnz},
+                   "row_order": args.row_order, "iterations_per_step": iters, "nrows": n, "nnz": nnz,
+                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3)},
         "roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
                      "traffic": None, "algorithmic_bytes_per_iteration": b_it},
@@ -758,6 +763,8 @@ def main():
     p.add_argument("--kernel", default=None)
     p.add_argument("--threshold", type=int, default=0)
     p.add_argument("--permuted", action="store_true")
+    p.add_argument("--row-order", choices=["reference", "locality"], default=None,
+                   help="r/rs kernels: reference sort_rows_desc order or the locality (Cuthill-McKee) order")
     p.add_argument("--scale", type=float, default=1.0, help="mesh edge scale (tests only)")
     p.add_argument("--iterations", type=int, default=1000)
     p.add_argument("--cpu-cg-iters", type=int, default=20)
@@ -772,6 +779,8 @@ def main():
         args.permuted = args.permuted or args.kernel.endswith(("r", "rs"))
     if args.steps is None:
         args.steps = 3 if args.workload == "cg" else 2000
+    if args.row_order is None:
+        args.row_order = "reference"
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         out = run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))

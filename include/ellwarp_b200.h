@@ -71,7 +71,16 @@ typedef struct ew_warp_config {
 typedef struct ew_kernel_options {
     int64_t k2_threshold; /* <= 0: max row length (kernels.cpp:16-21) */
     int64_t hyb_k_ell;    /* < 0: 2/3 coverage heuristic */
+    /* Row order of the r / rs kernels (extension; the reference has only
+     * EW_ROW_ORDER_REFERENCE). EW_ROW_ORDER_LOCALITY: the stable longest-first
+     * sort is applied to a Cuthill-McKee order instead of the row ids, so
+     * mesh neighbours share a warp; every row keeps the reference's entry
+     * order (same row sums), the permutation -- and apply_permuted's
+     * numbering -- is that order. */
+    int64_t row_order;
 } ew_kernel_options;
+
+enum { EW_ROW_ORDER_REFERENCE = 0, EW_ROW_ORDER_LOCALITY = 1 };
 
 /* CgConfig (cg.hpp:10-18) */
 typedef struct ew_cg_config {

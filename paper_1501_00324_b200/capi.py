@@ -57,7 +57,10 @@ class WarpConfig(C.Structure):
 
 
 class KernelOptions(C.Structure):
-    _fields_ = [("k2_threshold", C.c_int64), ("hyb_k_ell", C.c_int64)]
+    _fields_ = [("k2_threshold", C.c_int64), ("hyb_k_ell", C.c_int64), ("row_order", C.c_int64)]
+
+
+ROW_ORDERS = {"reference": 0, "locality": 1}
 
 
 class CgConfig(C.Structure):
@@ -481,9 +484,12 @@ class Kernel:
     """PreparedKernel (kernels.hpp:16-23) over device data (ew_kernel)."""
 
     def __init__(self, kernel_id, csr: Csr, warp_size=32, threshold=0, segment_bytes=128, align=True,
-                 block_size=None, hyb_k_ell=-1):
+                 block_size=None, hyb_k_ell=-1, row_order="reference"):
+        """row_order="locality" (r / rs ids only): rows grouped into warps by a
+        Cuthill-McKee order before the longest-first sort; same row sums,
+        perm() / apply_permuted() in that order (ew_kernel_options.row_order)."""
         cfg = WarpConfig.make(warp_size, block_size=block_size, segment_bytes=segment_bytes, align=align)
-        opts = KernelOptions(int(threshold), int(hyb_k_ell))
+        opts = KernelOptions(int(threshold), int(hyb_k_ell), ROW_ORDERS[row_order])
         h = C.c_void_p()
         check(lib().ew_kernel_prepare(kernel_id.encode(), csr.h, C.byref(cfg), C.byref(opts), C.byref(h)))
         self.h = h
@@ -669,7 +675,7 @@ class Dist:
         ro, ci, v = (_host(m.row_offsets, np.int64), _host(m.col_indices, np.int64), _host(m.values, np.float64))
         b = _host(bounds, np.int64) if bounds is not None else None
         cfg = WarpConfig.make(warp_size)
-        opts = KernelOptions(int(threshold), -1)
+        opts = KernelOptions(int(threshold), -1, 0)
         idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
         h = C.c_void_p()
         check(lib().ew_dist_create(m.nrows, m.ncols, ro.size, _ptr(ro), ci.size, _ptr(ci), _ptr(v), _ptr(b),
@@ -691,7 +697,7 @@ class Dist:
         ro, ci, v = _host(ro, np.int64), _host(ci, np.int64), _host(v, np.float64)
         b = _host(bounds, np.int64)
         cfg = WarpConfig.make(warp_size)
-        opts = KernelOptions(int(threshold), -1)
+        opts = KernelOptions(int(threshold), -1, 0)
         idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
         h = C.c_void_p()
         check(lib().ew_dist_create_block(int(nglobal), ro.size - 1, _ptr(ro), _ptr(ci), _ptr(v), _ptr(b),

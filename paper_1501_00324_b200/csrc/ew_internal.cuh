@@ -158,6 +158,7 @@ struct KernelData {
     std::string id;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored_slots = 0;
     bool reordered = false;  // r / rs variants: perm set, apply permutes in/out
+    bool locality = false;   // EW_ROW_ORDER_LOCALITY: perm is the locality order
     std::shared_ptr<CsrData> csr;        // csr_ref, and the arrays of csr_vector / coo
     std::shared_ptr<LayoutData> layout;  // k1* / k2*
     std::shared_ptr<FormatData> format;  // csr_vector / coo / ell / hyb
@@ -187,6 +188,13 @@ void sort_rows_desc(const CsrData& m, int32_t* fwd, int32_t* inv, int32_t* slen,
 std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool renumber,
                                  bool sort_within_rows, int32_t* fwd_out, cudaStream_t s,
                                  DevBuf<int64_t>* dst_of = nullptr);
+// Locality row order (ew_order.cu): a Cuthill-McKee BFS order of m's rows,
+// and the operand of a locality-ordered r / rs kernel: op (reorder() output,
+// P-numbered columns, m's row offsets) with its rows permuted into
+// qf = stable longest-first sort of that order and columns renumbered to qi.
+void locality_order(const CsrData& m, int32_t* order, cudaStream_t s);
+std::shared_ptr<CsrData> locality_operand(const CsrData& m, const CsrData& op, const int32_t* pf, int32_t* qf,
+                                          int32_t* qi, cudaStream_t s);
 void layout_refresh_values_reordered(LayoutData& l, const CsrData& m, const int64_t* dst_of, cudaStream_t s);
 // out[slot] = source entry of m for every slot of l (-1 for padding), mapped
 // through orig_of when given.

@@ -7,6 +7,10 @@ namespace ew {
 std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, const ew_warp_config& c,
                                     const ew_kernel_options& o, cudaStream_t s) {
     validate_config(c);  // prepare_kernel validates first (kernels.cpp:61)
+    require(o.row_order == EW_ROW_ORDER_REFERENCE || o.row_order == EW_ROW_ORDER_LOCALITY, "unknown row_order");
+    require(o.row_order == EW_ROW_ORDER_REFERENCE ||
+                (sid.size() > 2 && (sid.compare(0, 2, "k1") == 0 || sid.compare(0, 2, "k2") == 0)),
+            "row_order=locality needs an r / rs kernel id (k1r, k1rs, k2r, k2rs)");
     auto k = std::make_shared<KernelData>();
     k->id = sid;
     k->nrows = src.nrows;
@@ -25,13 +29,32 @@ std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, 
         const bool reordered = sid.size() > 2;
         // KernelOptions::k2_threshold <= 0: the max row length (kernels.cpp:16-21)
         const int64_t thr = o.k2_threshold > 0 ? o.k2_threshold : std::max<int64_t>(1, src.maxrow);
+        const bool locality = o.row_order == EW_ROW_ORDER_LOCALITY;
         std::shared_ptr<CsrData> op;
+        DevBuf<int32_t> qf, qi;
         if (reordered) {
             require(src.nrows == src.ncols, "kernel '" + sid + "' requires a square matrix");
             op = reorder(src, nullptr, true, sid.size() == 4, nullptr, s, &k->entry_dst);
+            if (locality) {
+                // rows regrouped by locality; each keeps op's (reference) entry order
+                const int64_t n = src.nrows;
+                DevBuf<int32_t> pf(n), pi(n), sl(n);
+                sort_rows_desc(src, pf.get(), pi.get(), sl.get(), s, nullptr);
+                qf.alloc(n);
+                qi.alloc(n);
+                op = locality_operand(src, *op, pf.get(), qf.get(), qi.get(), s);
+            }
         }
         k->reordered = reordered;
+        k->locality = locality;
         k->layout = build_layout(reordered ? *op : src, is_k2 ? EW_LAYOUT_K2 : EW_LAYOUT_K1, c, thr, true, false, s);
+        if (locality && src.nrows) {
+            // op's rows are already longest-first, so the layout's own sort is
+            // the identity; its permutation is the locality order
+            EW_CUDA_CHECK(cudaMemcpyAsync(k->layout->fwd.get(), qf.get(), src.nrows * 4, cudaMemcpyDeviceToDevice, s));
+            EW_CUDA_CHECK(cudaMemcpyAsync(k->layout->inv.get(), qi.get(), src.nrows * 4, cudaMemcpyDeviceToDevice, s));
+            EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
         k->stored_slots = k->layout->stored_slots;
     } else {
         throw Error(EW_INVALID_ARGUMENT, "unknown kernel id '" + sid + "'");
