@@ -444,8 +444,8 @@ def run_cg_dist(args, rank, world, local):
     diag[rows[hit]] = v[hit]
     dd = torch.tensor(diag, device="cuda")
     iters = args.iterations
-    for _ in range(max(1, args.warmup // 3)):
-        d.cg_solve(b, dd, tol=1e-300, max_iterations=10)
+    for _ in range(args.warmup):  # full-length steps: clocks ramp up from idle
+        d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
     torch.cuda.synchronize()
     barrier(world)
     l0 = capi.launch_count()
@@ -507,8 +507,8 @@ def run_cg(args, rank, world, local):
     bd = torch.tensor(b, device="cuda")
     dd = torch.tensor(diag, device="cuda")
     iters = args.iterations
-    for _ in range(args.warmup):
-        k.cg_solve(bd, dd, tol=1e-300, max_iterations=20, permuted=args.permuted)
+    for _ in range(args.warmup):  # full-length steps: clocks ramp up from idle
+        k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
     torch.cuda.synchronize()
     barrier(world)
     l0 = capi.launch_count()
@@ -780,7 +780,9 @@ def main():
     if args.steps is None:
         args.steps = 3 if args.workload == "cg" else 2000
     if args.row_order is None:
-        args.row_order = "reference"
+        # CG on an r / rs kernel: the locality row order (same row sums,
+        # EW_ROW_ORDER_LOCALITY); everything else the reference's order
+        args.row_order = "locality" if args.workload == "cg" and args.kernel.endswith(("r", "rs")) else "reference"
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         out = run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))

@@ -28,9 +28,13 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
     require(cfg.max_iterations >= 0, "cg: max_iterations must be >= 0");
 
     DevBuf<double> r(n), p(n), q(n), hist(cfg.max_iterations + 1);
-    // CG reductions use 2 x kRedGridMax partials; the SpMV-fused p.q one per SpMV CTA
-    const size_t npart = std::max<size_t>(2 * cg::kRedGridMax, static_cast<size_t>((n + 255) / 256));
+    // CG reductions use 2 x kRedGridMax partials; the SpMV-fused p.q a
+    // two-level grid sum over one CTA per 256 rows
+    const int64_t spmv_blocks = (n + 255) / 256;
+    const size_t npart = std::max<size_t>(2 * cg::kRedGridMax, cg::grid_sum_partials(spmv_blocks));
     DevBuf<double> partials(npart);
+    DevBuf<unsigned> tickets(std::max<size_t>(1, cg::grid_sum_tickets(spmv_blocks)));
+    EW_CUDA_CHECK(cudaMemsetAsync(tickets.get(), 0, tickets.bytes(), s));
     DevBuf<State> st(1);
     EW_CUDA_CHECK(cudaMemsetAsync(st.get(), 0, sizeof(State), s));
     if (n) EW_CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
@@ -90,24 +94,25 @@ CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, i
                     stop = true;
                     break;
                 }
-                if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), static_cast<unsigned>(npart), st.get(), 0})) {
+                if (!op.apply_dot(p.get(), q.get(), s, done, DotSink{partials.get(), static_cast<unsigned>(npart), tickets.get(), st.get(), 0})) {
                     op.apply(p.get(), q.get(), s, done);
-                    cg::pq_kernel<false><<<g_pq, cg::kRedBlock, 0, s>>>(p.get(), q.get(), n, partials.get(), st.get());
+                    launch_pdl(cg::pq_kernel<false>, g_pq, cg::kRedBlock, s, p.get(), q.get(), n, partials.get(),
+                               st.get());
                     launched("cg::pq_kernel");
                 }
                 const bool refresh = interval > 0 && it % interval == 0;
-                cg::update_kernel<false><<<g_up, cg::kRedBlock, 0, s>>>(
-                    refresh ? 1 : 0, x, r.get(), p.get(), q.get(), b, diag, n, jacobi, it, cfg.rel_tolerance,
-                    cfg.divergence_limit, partials.get(), st.get(), hist.get());
+                launch_pdl(cg::update_kernel<false>, g_up, cg::kRedBlock, s, refresh ? 1 : 0, x, r.get(), p.get(),
+                           q.get(), b, diag, n, jacobi, (long long)it, cfg.rel_tolerance, cfg.divergence_limit,
+                           partials.get(), st.get(), hist.get());
                 launched("cg::update_kernel");
                 if (refresh) {
                     if (!(host_op && host_done())) op.apply(x, q.get(), s, done);
-                    cg::update_kernel<false><<<g_up, cg::kRedBlock, 0, s>>>(
-                        2, x, r.get(), p.get(), q.get(), b, diag, n, jacobi, it, cfg.rel_tolerance,
-                        cfg.divergence_limit, partials.get(), st.get(), hist.get());
+                    launch_pdl(cg::update_kernel<false>, g_up, cg::kRedBlock, s, 2, x, r.get(), p.get(), q.get(), b,
+                               diag, n, jacobi, (long long)it, cfg.rel_tolerance, cfg.divergence_limit,
+                               partials.get(), st.get(), hist.get());
                     launched("cg::update_kernel");
                 }
-                cg::p_kernel<<<gs, 256, 0, s>>>(p.get(), r.get(), diag, n, jacobi, st.get());
+                launch_pdl(cg::p_kernel, gs, 256, s, p.get(), r.get(), diag, n, jacobi, (const cg::State*)st.get());
                 launched("cg::p_kernel");
             }
             // poll the previous batch's state while this batch runs

@@ -79,18 +79,75 @@ __device__ __forceinline__ bool publish_partials(const double (&v)[NV], double* 
 
 template <int NV>
 __device__ __forceinline__ void final_sum(double (&out)[NV], const double* partials) {
+    // Thread t sums partials t, t + blockDim, ... in that order; the loads
+    // are issued together (L2, past L1) rather than one dependent load per
+    // step. Grids are at most kRedGridMax CTAs.
+    constexpr int kMaxPer = (kRedGridMax + kRedBlock - 1) / kRedBlock;
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
+        double ld[kMaxPer];
+#pragma unroll
+        for (int u = 0; u < kMaxPer; ++u) {
+            const int b = threadIdx.x + u * blockDim.x;
+            ld[u] = b < (int)gridDim.x ? __ldcg(&partials[i * gridDim.x + b]) : 0.0;
+        }
         double t = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-            t = __dadd_rn(t, *((volatile const double*)&partials[i * gridDim.x + b]));
+#pragma unroll
+        for (int u = 0; u < kMaxPer; ++u)
+            if (threadIdx.x + u * blockDim.x < gridDim.x) t = __dadd_rn(t, ld[u]);
         v[i] = t;
     }
     block_sum<NV>(v);
 #pragma unroll
     for (int i = 0; i < NV; ++i) out[i] = v[i];
 }
+
+// Two-level deterministic grid sum for plain (one CTA per 256 rows) grids of
+// any size, finished inside the kernel: every CTA publishes its sum; the
+// last CTA of each group of kRedBlock CTAs sums the group in CTA order; the
+// last group to finish sums the group totals in group order. The order of
+// every addition is fixed by the grid shape alone. partials holds
+// gridDim.x + ngroups doubles, tickets ngroups zeroed counters (left zeroed).
+// True in thread 0 of the one CTA that holds the total.
+__device__ __forceinline__ bool grid_sum(double v, double* partials, unsigned* tickets, unsigned* top,
+                                         double& total) {
+    __shared__ bool last;
+    const unsigned G = gridDim.x, g = blockIdx.x / kRedBlock, ng = (G + kRedBlock - 1) / kRedBlock;
+    const unsigned gsize = min(static_cast<unsigned>(kRedBlock), G - g * kRedBlock);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(&tickets[g], 1u) == gsize - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    double t[1] = {threadIdx.x < gsize ? __ldcg(&partials[g * kRedBlock + threadIdx.x]) : 0.0};
+    block_sum<1>(t);
+    if (threadIdx.x == 0) {
+        tickets[g] = 0;
+        partials[G + g] = t[0];
+        __threadfence();
+        last = atomicAdd(top, 1u) == ng - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    double u[1] = {0.0};
+    for (unsigned i = threadIdx.x; i < ng; i += blockDim.x) u[0] = __dadd_rn(u[0], __ldcg(&partials[G + i]));
+    block_sum<1>(u);
+    if (threadIdx.x != 0) return false;
+    *top = 0;
+    total = u[0];
+    return true;
+}
+
+// partials / tickets a plain grid of `nblocks` CTAs needs for grid_sum
+inline size_t grid_sum_partials(int64_t nblocks) {
+    return static_cast<size_t>(nblocks + (nblocks + kRedBlock - 1) / kRedBlock);
+}
+inline size_t grid_sum_tickets(int64_t nblocks) { return static_cast<size_t>((nblocks + kRedBlock - 1) / kRedBlock); }
 
 // ---- decisions (cg.cpp), applied to global totals by one thread ----------
 __device__ __forceinline__ void decide_bnorm(State* st, double bb) { st->bnorm = sqrt(bb); }
@@ -220,6 +277,7 @@ constexpr int kUpdU = 2;  // the update kernel's divisions cost registers: two p
 template <bool DIST>
 __global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict__ p, const double* __restrict__ q,
                                                        int64_t n, double* partials, State* st) {
+    pdl_wait();
     if (st->done) return;
     double v[1] = {0.0};
     EW_ROUNDS(i0, S, n) {
@@ -234,6 +292,7 @@ __global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict_
         for (int u = 0; u < kU; ++u)
             if (i0 + u * S < n) v[0] = __dadd_rn(v[0], __dmul_rn(a[u], c[u]));
     }
+    pdl_trigger();
     finish<DIST, 1>(v, partials, st, [&](const double (&t)[1]) { decide_pq(st, t[0]); });
 }
 
@@ -247,6 +306,7 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
                                                            const double* __restrict__ diag, int64_t n, int jacobi,
                                                            long long k, double tol, double divergence,
                                                            double* partials, State* st, double* hist) {
+    pdl_wait();
     if (st->done) return;
     const double alpha = st->alpha;
     double v[2] = {0.0, 0.0};
@@ -278,6 +338,7 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
             v[1] = __dadd_rn(v[1], __dmul_rn(ri, zi));
         }
     }
+    pdl_trigger();
     if (mode == 1) return;
     if (bad) atomicOr(&st->flags, 1);
     finish<DIST, 2>(v, partials, st, [&](const double (&t)[2]) {
@@ -289,6 +350,7 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
 static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, const double* __restrict__ r,
                                                 const double* __restrict__ diag, int64_t n, int jacobi,
                                                 const State* st) {
+    pdl_wait();
     if (st->done) return;
     const double beta = st->beta;
     EW_ROUNDS(i0, S, n) {
@@ -309,31 +371,7 @@ static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, c
             p[i] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
         }
     }
-}
-
-// Ends the SpMV-fused p.q: one CTA sums the per-CTA partials of
-// k1_dot_kernel in a fixed order, then decides (or stores the partition
-// total for a partitioned solve).
-static __global__ void __launch_bounds__(1024) dot_final_kernel(const double* __restrict__ partials, unsigned n,
-                                                                State* st, int dist) {
-    if (st->done) return;
-    __shared__ double sh[32];
-    double t = 0.0;
-    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) t = __dadd_rn(t, partials[i]);
-    t = warp_sum(t);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        t = warp_sum(threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0);
-        if (threadIdx.x == 0) {
-            if (dist) {
-                st->loc[0] = t;
-                st->loc[1] = 0.0;
-            } else {
-                decide_pq(st, t);
-            }
-        }
-    }
+    pdl_trigger();
 }
 
 // DIST: sum the all-gathered partition totals in rank order, then decide.

@@ -114,6 +114,7 @@ struct DistPart {
     std::shared_ptr<KernelData> op;
     // CG / SpMV buffers (ext = owned + ghost tail)
     DevBuf<double> x_ext, p_ext, r, q, b, diag, hist, partials, gathered;
+    DevBuf<unsigned> tickets;  // SpMV-fused p.q grid sum (cg::grid_sum)
     DevBuf<cg::State> st;
 };
 
@@ -420,7 +421,10 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         P->b.alloc(n);
         P->diag.alloc(jacobi ? n : 0);
         P->hist.alloc(cfg.max_iterations + 1);
-        P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, static_cast<size_t>((n + 255) / 256)));
+        const int64_t spmv_blocks = (n + 255) / 256;
+        P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, cg::grid_sum_partials(spmv_blocks)));
+        P->tickets.alloc(std::max<size_t>(1, cg::grid_sum_tickets(spmv_blocks)));
+        EW_CUDA_CHECK(cudaMemsetAsync(P->tickets.get(), 0, P->tickets.bytes(), s));
         P->st.alloc(1);
         EW_CUDA_CHECK(cudaMemsetAsync(P->st.get(), 0, sizeof(cg::State), s));
         if (ne) {
@@ -506,7 +510,8 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                 for (auto& P : D.parts) {
                     const int* done = &P->st.get()->done;
                     if (kernel_apply_dot(*P->op, P->p_ext.get(), P->q.get(), false, s, done,
-                                         DotSink{P->partials.get(), static_cast<unsigned>(P->partials.size()), P->st.get(), 1}))
+                                         DotSink{P->partials.get(), static_cast<unsigned>(P->partials.size()), P->tickets.get(),
+                                                 P->st.get(), 1}))
                         continue;
                     kernel_apply(*P->op, P->p_ext.get(), P->q.get(), false, s, done);
                     cg::pq_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(

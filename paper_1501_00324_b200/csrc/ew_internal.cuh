@@ -41,6 +41,31 @@ inline void launched(const char* what) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while the previous kernel on the stream drains; it must call
+// pdl_wait() before touching anything that kernel wrote. Kernels on the CG
+// path call pdl_trigger() on entry so their successor can launch early. Both
+// are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // EW_PDL=0 disables the attribute (A/B runs)
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+}
+
 // Owning device allocation (cudaMalloc; long-lived data: matrices, layouts).
 template <typename T>
 class DevBuf {
@@ -224,8 +249,9 @@ namespace cg {
 struct State;
 }
 struct DotSink {
-    double* partials;   // one partial per SpMV CTA
+    double* partials;   // cg::grid_sum_partials(SpMV CTAs)
     unsigned capacity;  // partials' length; a larger grid falls back to the dot kernel
+    unsigned* tickets;  // cg::grid_sum_tickets(SpMV CTAs) zeroed counters
     cg::State* st;      // decision / partition total
     int dist;           // 1: store the partition total in st->loc
 };

@@ -1,8 +1,18 @@
 // Prepared kernels: prepare_kernel / apply / apply_permuted (kernels.cpp:14-125)
 // over device layouts.
+#include <cstdlib>
+
 #include "ew_internal.cuh"
 
 namespace ew {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("EW_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 std::shared_ptr<KernelData> prepare(const std::string& sid, const CsrData& src, const ew_warp_config& c,
                                     const ew_kernel_options& o, cudaStream_t s) {

@@ -111,6 +111,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
 // SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
 template <bool SORTED, bool SCATTER, bool ROW_MAJOR>
 __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
+    pdl_wait();
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= a.nrows || (a.done && *a.done)) return;
     const uint64_t pol = evict_first_policy();
@@ -124,15 +125,16 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
         sum = lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
     }
     a.y[SCATTER ? a.fwd[p] : p] = sum;
+    pdl_trigger();
 }
 
 // K1 with the CG's p.q fused in (cg.cpp:72): the operator input x is p, so
-// each row adds x[target] * y[target] to a deterministic grid reduction
-// whose last CTA applies the breakdown test and alpha = rz / pq (or, for a
-// partitioned solve, stores the partition total). Grid-stride over rows so
-// the partial count stays at most cg::kRedGridMax.
+// each row adds x[target] * y[target] to a deterministic two-level grid sum
+// (cg::grid_sum) whose last CTA applies the breakdown test and
+// alpha = rz / pq (or, for a partitioned solve, stores the partition total).
 template <bool SORTED, bool SCATTER>
-__global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
+__global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, DotSink sink) {
+    pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double v[1] = {0.0};
@@ -149,8 +151,16 @@ __global__ void __launch_bounds__(256) k1_dot_kernel(K1Args a, double* __restric
         a.y[t] = sum;
         v[0] = __dmul_rn(a.x[t], sum);
     }
-    cg::block_sum<1>(v);  // fixed tree; one partial per CTA, summed by cg::dot_final_kernel
-    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+    pdl_trigger();
+    cg::block_sum<1>(v);  // fixed tree per CTA
+    double total;
+    if (!cg::grid_sum(v[0], sink.partials, sink.tickets, &sink.st->ticket, total)) return;
+    if (sink.dist) {
+        sink.st->loc[0] = total;
+        sink.st->loc[1] = 0.0;
+    } else {
+        cg::decide_pq(sink.st, total);
+    }
 }
 
 struct K2Args {
@@ -178,6 +188,7 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t w = t >> a.ws_log2;
     const int32_t lane = static_cast<int32_t>(t & (a.ws - 1));
+    pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const uint64_t pol = evict_first_policy();
     double sum = 0.0;
@@ -202,6 +213,7 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a) {
         if (st < red && (tl & (2 * st - 1)) == 0) sum = __dadd_rn(sum, o);
     }
     if (leader) a.y[SCATTER ? a.fwd[pos] : pos] = sum;
+    pdl_trigger();
 }
 
 // K2 for warp_size in (32, 1024]: one CTA of ws threads per layout warp, the
@@ -235,9 +247,9 @@ __global__ void k2_wide_kernel(K2Args a) {
 template <bool SORTED, bool SCATTER>
 void launch_k1(const K1Args& a, bool row_major, cudaStream_t s) {
     if (row_major)
-        k1_kernel<SORTED, SCATTER, true><<<grid_for(a.nrows), kBlock, 0, s>>>(a);
+        launch_pdl(k1_kernel<SORTED, SCATTER, true>, grid_for(a.nrows), kBlock, s, a);
     else
-        k1_kernel<SORTED, SCATTER, false><<<grid_for(a.nrows), kBlock, 0, s>>>(a);
+        launch_pdl(k1_kernel<SORTED, SCATTER, false>, grid_for(a.nrows), kBlock, s, a);
     launched("k1_kernel");
 }
 
@@ -245,7 +257,7 @@ template <bool SORTED, bool SCATTER>
 void launch_k2(const K2Args& a, cudaStream_t s) {
     if (a.nwarps == 0) return;
     if (a.ws <= 32) {
-        k2_kernel<SORTED, SCATTER><<<grid_for(a.nwarps * a.ws), kBlock, 0, s>>>(a);
+        launch_pdl(k2_kernel<SORTED, SCATTER>, grid_for(a.nwarps * a.ws), kBlock, s, a);
     } else {
         k2_wide_kernel<SORTED, SCATTER><<<static_cast<unsigned>(a.nwarps), a.ws, a.ws * sizeof(double), s>>>(a);
     }
@@ -260,16 +272,14 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
     const unsigned grid = grid_for(l.nrows);
-    if (grid > sink.capacity) return false;
-    auto go = [&](auto kernel) { kernel<<<grid, 256, 0, s>>>(a, sink.partials); };
+    if (cg::grid_sum_partials(grid) > sink.capacity) return false;
+    auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink); };
     if (l.sorted) {
         scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
     } else {
         scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
     }
     launched("k1_dot_kernel");
-    cg::dot_final_kernel<<<1, 1024, 0, s>>>(sink.partials, grid, sink.st, sink.dist);
-    launched("cg::dot_final_kernel");
     return true;
 }
 
