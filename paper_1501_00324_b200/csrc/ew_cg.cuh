@@ -217,6 +217,7 @@ __device__ __forceinline__ void finish(const double (&v)[NV], double* partials, 
         if (DIST) {
 #pragma unroll
             for (int i = 0; i < NV; ++i) st->loc[i] = tot[i];
+            if (NV == 1) st->loc[1] = 0.0;  // p.q: the second row-set slot
         } else {
             decide(tot);
         }
@@ -386,7 +387,7 @@ static __global__ void finalize_kernel(int what, const double* __restrict__ gath
     switch (what) {
         case kBnorm: decide_bnorm(st, t0); break;
         case kStart: decide_start(st, t0, t1, tol, hist); break;
-        case kPq: decide_pq(st, t0); break;
+        case kPq: decide_pq(st, __dadd_rn(t0, t1)); break;  // interior + boundary row sets
         default: decide_update(st, t0, t1, k, tol, divergence, hist); break;
     }
 }

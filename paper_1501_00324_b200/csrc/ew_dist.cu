@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -112,6 +113,11 @@ struct DistPart {
     DevBuf<double> send_buf;
     std::shared_ptr<CsrData> local;
     std::shared_ptr<KernelData> op;
+    // Overlap (K1, G > 1): op_int holds the rows without ghost columns and
+    // runs while the halo is in flight, op_bnd the rest once it has landed.
+    // Both layouts scatter straight into local row ids; op is then unused.
+    std::shared_ptr<KernelData> op_int, op_bnd;
+    int64_t n_int = 0, n_bnd = 0;
     // CG / SpMV buffers (ext = owned + ghost tail)
     DevBuf<double> x_ext, p_ext, r, q, b, diag, hist, partials, gathered;
     DevBuf<unsigned> tickets;  // SpMV-fused p.q grid sum (cg::grid_sum)
@@ -125,7 +131,13 @@ struct DistData {
     bool use_nccl = false;
     ncclComm_t comm = nullptr;
     std::string kernel_id;
+    bool split = false;                    // every part has op_int / op_bnd
+    cudaStream_t comm_stream = nullptr;    // halo exchange, concurrent with the interior rows
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ~DistData() {
+        if (ev_ready) cudaEventDestroy(ev_ready);
+        if (ev_halo) cudaEventDestroy(ev_halo);
+        if (comm_stream) cudaStreamDestroy(comm_stream);
         if (comm) nccl().CommDestroy(comm);
     }
 };
@@ -146,6 +158,45 @@ std::vector<int64_t> ghost_list(const int64_t* bro, const int64_t* bci, int64_t 
 
 int32_t owner_of(const std::vector<int64_t>& bounds, int64_t c) {
     return static_cast<int32_t>(std::upper_bound(bounds.begin(), bounds.end(), c) - bounds.begin() - 1);
+}
+
+// Interior / boundary split for K1 when there is a halo to hide
+// (EW_DIST_OVERLAP=0 turns it off for A/B runs).
+bool split_rows(const std::string& kid, int32_t G) {
+    static const bool on = [] {
+        const char* e = std::getenv("EW_DIST_OVERLAP");
+        return !(e && e[0] == '0');
+    }();
+    return on && G > 1 && kid == "k1";
+}
+
+// K1 kernel over a subset of the local rows (ascending local ids), entries
+// in their order, its layout scattering into local row ids.
+std::shared_ptr<KernelData> prepare_rows(const std::vector<int64_t>& rows, const std::vector<int64_t>& lro,
+                                         const std::vector<int64_t>& lci, const double* lv, int64_t ncols,
+                                         const std::string& kid, const ew_warp_config& cfg,
+                                         const ew_kernel_options& opts, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(rows.size());
+    std::vector<int64_t> sro(n + 1, 0), sci;
+    std::vector<double> sv;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = rows[i];
+        sci.insert(sci.end(), lci.begin() + lro[r], lci.begin() + lro[r + 1]);
+        sv.insert(sv.end(), lv + lro[r], lv + lro[r + 1]);
+        sro[i + 1] = static_cast<int64_t>(sci.size());
+    }
+    auto sub = csr_upload(n, ncols, n + 1, sro.data(), static_cast<int64_t>(sci.size()), sci.data(), sv.data(),
+                          EW_MEM_HOST, false, s);
+    auto k = prepare(kid, *sub, cfg, opts, s);
+    if (n) {
+        std::vector<int32_t> f(static_cast<size_t>(n));
+        EW_CUDA_CHECK(cudaMemcpyAsync(f.data(), k->layout->fwd.get(), n * 4, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (auto& v : f) v = static_cast<int32_t>(rows[v]);
+        EW_CUDA_CHECK(cudaMemcpyAsync(k->layout->fwd.get(), f.data(), n * 4, cudaMemcpyHostToDevice, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    return k;
 }
 
 // Partition g from its row block (bro: offsets relative to the block,
@@ -181,9 +232,22 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
         lci[k] = (c >= P.r0 && c < P.r1) ? c - P.r0
                                          : P.nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), c) - ghosts.begin());
     }
-    P.local = csr_upload(P.nloc, P.nloc + P.nghost, P.nloc + 1, lro.data(), lnnz, lci.data(), bv + bro[0],
-                         EW_MEM_HOST, false, s);
-    P.op = prepare(kid, *P.local, cfg, opts, s);
+    if (split_rows(kid, G)) {
+        std::vector<int64_t> rows_int, rows_bnd;
+        for (int64_t r = 0; r < P.nloc; ++r) {
+            bool ghost = false;
+            for (int64_t k = lro[r]; k < lro[r + 1] && !ghost; ++k) ghost = lci[k] >= P.nloc;
+            (ghost ? rows_bnd : rows_int).push_back(r);
+        }
+        P.n_int = static_cast<int64_t>(rows_int.size());
+        P.n_bnd = static_cast<int64_t>(rows_bnd.size());
+        P.op_int = prepare_rows(rows_int, lro, lci, bv + bro[0], P.nloc + P.nghost, kid, cfg, opts, s);
+        P.op_bnd = prepare_rows(rows_bnd, lro, lci, bv + bro[0], P.nloc + P.nghost, kid, cfg, opts, s);
+    } else {
+        P.local = csr_upload(P.nloc, P.nloc + P.nghost, P.nloc + 1, lro.data(), lnnz, lci.data(), bv + bro[0],
+                             EW_MEM_HOST, false, s);
+        P.op = prepare(kid, *P.local, cfg, opts, s);
+    }
     P.send_idx.alloc(sidx.size());
     P.send_buf.alloc(sidx.size());
     if (!sidx.empty())
@@ -256,9 +320,73 @@ void finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaS
     }
 }
 
-void local_spmv(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, bool guard) {
-    for (auto& P : D.parts)
-        kernel_apply(*P->op, ((*P).*ext).get(), P->q.get(), false, s, guard ? &P->st.get()->done : nullptr);
+// The exchange on the comm stream, ordered after everything already on s.
+void halo_begin(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+    EW_CUDA_CHECK(cudaEventRecord(D.ev_ready, s));
+    EW_CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_ready, 0));
+    halo(D, ext, D.comm_stream);
+    EW_CUDA_CHECK(cudaEventRecord(D.ev_halo, D.comm_stream));
+}
+
+void halo_end(DistData& D, cudaStream_t s) { EW_CUDA_CHECK(cudaStreamWaitEvent(s, D.ev_halo, 0)); }
+
+// One row set of a split part; with `dot`, its p.q partial goes to loc[slot].
+// False when the fused dot was not available (the caller runs pq_kernel).
+bool run_rows(DistPart& P, const KernelData& k, int64_t nrows, int slot, const double* xe, cudaStream_t s,
+              const int* done, bool dot) {
+    if (!nrows) {
+        if (dot) EW_CUDA_CHECK(cudaMemsetAsync(P.st.get()->loc + slot, 0, (slot == 0 ? 2 : 1) * sizeof(double), s));
+        return true;
+    }
+    if (dot && kernel_apply_dot(k, xe, P.q.get(), false, s, done,
+                                DotSink{P.partials.get(), static_cast<unsigned>(P.partials.size()), P.tickets.get(),
+                                        P.st.get(), 1, slot}))
+        return true;
+    kernel_apply(k, xe, P.q.get(), false, s, done);
+    return !dot;
+}
+
+// q = A x_ext on every local partition after (or, split, overlapped with)
+// the halo exchange of `ext`; dot: p.q into each part's State::loc.
+void spmv_exchange(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, bool guard, bool dot,
+                   bool exchange = true) {
+    std::vector<char> fused(D.parts.size(), 1);
+    if (!D.split) {
+        if (exchange) halo(D, ext, s);
+        for (size_t i = 0; i < D.parts.size(); ++i) {
+            DistPart& P = *D.parts[i];
+            fused[i] = run_rows(P, *P.op, P.nloc, 0, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr, dot);
+        }
+    } else {
+        if (exchange) halo_begin(D, ext, s);
+        for (size_t i = 0; i < D.parts.size(); ++i) {
+            DistPart& P = *D.parts[i];
+            fused[i] = run_rows(P, *P.op_int, P.n_int, 0, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr, dot);
+        }
+        if (exchange) halo_end(D, s);
+        for (size_t i = 0; i < D.parts.size(); ++i) {
+            DistPart& P = *D.parts[i];
+            fused[i] &= run_rows(P, *P.op_bnd, P.n_bnd, 1, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr,
+                                 dot);
+        }
+    }
+    if (!dot) return;
+    for (size_t i = 0; i < D.parts.size(); ++i) {
+        if (fused[i]) continue;
+        DistPart& P = *D.parts[i];
+        cg::pq_kernel<true><<<cg::red_grid(P.nloc), cg::kRedBlock, 0, s>>>(((P).*ext).get(), P.q.get(), P.nloc,
+                                                                          P.partials.get(), P.st.get());
+        launched("cg::pq_kernel<dist>");
+    }
+}
+
+void init_overlap(DistData& D) {
+    D.split = !D.parts.empty();
+    for (auto& P : D.parts) D.split = D.split && P->op_int && P->op_bnd;
+    if (!D.split) return;
+    EW_CUDA_CHECK(cudaStreamCreateWithFlags(&D.comm_stream, cudaStreamNonBlocking));
+    EW_CUDA_CHECK(cudaEventCreateWithFlags(&D.ev_ready, cudaEventDisableTiming));
+    EW_CUDA_CHECK(cudaEventCreateWithFlags(&D.ev_halo, cudaEventDisableTiming));
 }
 
 }  // namespace
@@ -304,6 +432,7 @@ std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_
         build_part(*P, g, nparts, D->bounds, ro + D->bounds[g], ci, v, ghosts[g], needs, kid, cfg, opts, s);
         D->parts.push_back(std::move(P));
     }
+    init_overlap(*D);
     return D;
 }
 
@@ -372,6 +501,7 @@ std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro,
     auto P = std::make_unique<DistPart>();
     build_part(*P, rank, nparts, D->bounds, bro, bci, bv, ghosts, needs, kid, cfg, opts, s);
     D->parts.push_back(std::move(P));
+    init_overlap(*D);
     return D;
 }
 
@@ -399,8 +529,7 @@ void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s) {
             EW_CUDA_CHECK(cudaMemcpyAsync(P->x_ext.get(), x + off, P->nloc * 8, cudaMemcpyDeviceToDevice, s));
         off += P->nloc;
     }
-    halo(D, &DistPart::x_ext, s);
-    local_spmv(D, &DistPart::x_ext, s, false);
+    spmv_exchange(D, &DistPart::x_ext, s, false, false);
     off = 0;
     for (auto& P : D.parts) {
         if (P->nloc) EW_CUDA_CHECK(cudaMemcpyAsync(y + off, P->q.get(), P->nloc * 8, cudaMemcpyDeviceToDevice, s));
@@ -478,7 +607,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         return out;
     }
     // r = b - A x0 (x0 = 0; the operator still runs, cg.cpp:52-57)
-    local_spmv(D, &DistPart::x_ext, s, false);
+    spmv_exchange(D, &DistPart::x_ext, s, false, false, /*exchange=*/false);  // x0 = 0 everywhere
     for (auto& P : D.parts) {
         cg::start_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
             P->b.get(), P->diag.get(), P->q.get(), P->r.get(), P->p_ext.get(), P->nloc, jacobi, cfg.rel_tolerance,
@@ -506,27 +635,13 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         while (it <= cfg.max_iterations) {
             const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
             for (; it <= last; ++it) {
-                halo(D, &DistPart::p_ext, s);
-                for (auto& P : D.parts) {
-                    const int* done = &P->st.get()->done;
-                    if (kernel_apply_dot(*P->op, P->p_ext.get(), P->q.get(), false, s, done,
-                                         DotSink{P->partials.get(), static_cast<unsigned>(P->partials.size()), P->tickets.get(),
-                                                 P->st.get(), 1}))
-                        continue;
-                    kernel_apply(*P->op, P->p_ext.get(), P->q.get(), false, s, done);
-                    cg::pq_kernel<true><<<cg::red_grid(P->nloc), cg::kRedBlock, 0, s>>>(
-                        P->p_ext.get(), P->q.get(), P->nloc, P->partials.get(), P->st.get());
-                    launched("cg::pq_kernel<dist>");
-                }
+                spmv_exchange(D, &DistPart::p_ext, s, true, true);
                 allgather(D, s);
                 finalize(D, cg::kPq, it, cfg, s);
                 const bool refresh = cfg.recompute_interval > 0 && it % cfg.recompute_interval == 0;
                 for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
                     if (mode < 0) break;
-                    if (mode == 2) {
-                        halo(D, &DistPart::x_ext, s);
-                        local_spmv(D, &DistPart::x_ext, s, true);
-                    }
+                    if (mode == 2) spmv_exchange(D, &DistPart::x_ext, s, true, false);
                     for (auto& P : D.parts) {
                         cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock,
                                                                     P->nloc),

@@ -253,7 +253,8 @@ struct DotSink {
     unsigned capacity;  // partials' length; a larger grid falls back to the dot kernel
     unsigned* tickets;  // cg::grid_sum_tickets(SpMV CTAs) zeroed counters
     cg::State* st;      // decision / partition total
-    int dist;           // 1: store the partition total in st->loc
+    int dist;           // 1: store the partition total in st->loc[slot]
+    int slot = 0;       // DIST: 0 (also clears loc[1]) or 1 (a second row set)
 };
 // K1 SpMV with p.q fused (x is p); false when the layout has no fused path.
 bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,

@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, DotSink sink) 
     double total;
     if (!cg::grid_sum(v[0], sink.partials, sink.tickets, &sink.st->ticket, total)) return;
     if (sink.dist) {
-        sink.st->loc[0] = total;
-        sink.st->loc[1] = 0.0;
+        sink.st->loc[sink.slot] = total;
+        if (sink.slot == 0) sink.st->loc[1] = 0.0;
     } else {
         cg::decide_pq(sink.st, total);
     }
