@@ -6,6 +6,20 @@ namespace ew {
 
 std::atomic<int64_t> g_launches{0};
 
+void retain_pool() {
+    static std::atomic<uint64_t> done_mask{0};  // one bit per device ordinal (< 64)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    const uint64_t bit = uint64_t{1} << dev;
+    if (done_mask.load(std::memory_order_relaxed) & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~uint64_t{0};
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_mask.fetch_or(bit, std::memory_order_relaxed);
+}
+
 namespace {
 
 enum : int { kBadOrder = 1, kBadColumn = 2, kNotIncreasing = 4 };

@@ -103,12 +103,20 @@ class DevBuf {
     size_t n_ = 0;
 };
 
+// Keeps freed scratch in the current device's default memory pool instead of
+// returning it to the driver at every synchronisation (the default release
+// threshold is 0: each call would re-map its scratch, ~0.1 ms).
+void retain_pool();
+
 // Stream-ordered scratch (cudaMallocAsync from the device's default pool).
 template <typename T>
 class Scratch {
   public:
     Scratch(size_t n, cudaStream_t s) : s_(s), n_(n) {
-        if (n) EW_CUDA_CHECK(cudaMallocAsync(&p_, n * sizeof(T), s));
+        if (n) {
+            retain_pool();
+            EW_CUDA_CHECK(cudaMallocAsync(&p_, n * sizeof(T), s));
+        }
     }
     ~Scratch() {
         if (p_) cudaFreeAsync(p_, s_);

@@ -66,7 +66,9 @@ struct K1Args {
 
 // Serial lane sum over j in [0, mx) at stride `step` from slot s, unrolled by
 // 8 so eight value/column loads and then eight x gathers are in flight per
-// thread before the (order-preserving) accumulation chain consumes them.
+// thread before the (order-preserving) accumulation chain consumes them; the
+// last mx % 4 steps go in one predicated block (two round trips, not two per
+// step).
 __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
                                            const int32_t* __restrict__ cols,
                                            const double* __restrict__ x, int64_t s, int64_t step,
@@ -100,9 +102,23 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
         s += 4 * step;
         j += 4;
     }
-    for (; j < mx; ++j) {
-        sum = madd(sum, ld_stream(vals + s, pol), ld_x(x, ld_stream(cols + s, pol)));
-        s += step;
+    // last 0..3 steps predicated, so their loads are in flight together too
+    const int32_t rem = mx - j;
+    if (rem > 0) {
+        int32_t c[3];
+        double v[3], xv[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) c[u] = ld_stream(cols + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) xv[u] = ld_x(x, c[u]);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) sum = madd(sum, v[u], xv[u]);
     }
     return sum;
 }
