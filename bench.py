@@ -235,19 +235,32 @@ def build_slab(args, rank, world):
 
 
 def dist_operator(args, rank, world):
+    """This rank's partition of the slab operator. Transport "ipc" (default):
+    CUDA IPC peer stores + mailboxes over NVLink, no NCCL on the data path;
+    "nccl": ncclSend/Recv halos and ncclAllGather dots."""
     import torch.distributed as dist
 
     from paper_1501_00324_b200 import capi
 
     ng, ro, ci, v, bounds = build_slab(args, rank, world)
-    obj = [capi.nccl_unique_id() if rank == 0 else None]
-    if world > 1:
-        dist.broadcast_object_list(obj, src=0)
+    kid = args.kernel if args.kernel in ("k1", "k2", "csr_ref") else "k1"
     t = time.time()
-    d = capi.Dist.block(ng, ro, ci, v, bounds, rank, obj[0], kernel=args.kernel if args.kernel in
-                        ("k1", "k2", "csr_ref") else "k1")
+    transport = args.transport
+    d = None
+    if transport == "ipc":
+        try:
+            d = capi.Dist.block_ipc(ng, ro, ci, v, bounds, rank, kernel=kid)
+        except (capi.DeviceError, ValueError) as e:
+            log(f"[bench] rank {rank}: IPC transport unavailable ({e}); falling back to NCCL")
+            transport = "nccl"
+    if d is None:
+        obj = [capi.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        d = capi.Dist.block(ng, ro, ci, v, bounds, rank, obj[0], kernel=kid)
+    args.transport_used = transport
     info = d.info()
-    log(f"[bench] rank {rank}: partitioned operator in {time.time() - t:.2f}s, {info['nghost']} ghosts, "
+    log(f"[bench] rank {rank}: partitioned operator ({transport}) in {time.time() - t:.2f}s, {info['nghost']} ghosts, "
         f"{info['nsend']} sent per exchange")
     return d, ng, ro, ci, v, info
 
@@ -414,7 +427,8 @@ def run_spmv_dist(args, rank, world, local):
         "data": "synthetic (seeded structured tet mesh, P1 elasticity element matrices)",
         "config": {"workload": f"row-partitioned fp64 SpMV, elasticity box slab of 87 node layers per GPU "
                                f"({nloc} rows/GPU)", "config": "c2-per-gpu", "kernel": "k1",
-                   "partition": "z-slab row blocks, halo exchange ncclSend/Recv + local K1",
+                   "partition": "z-slab row blocks; interior rows overlap the halo exchange, boundary rows after",
+                   "transport": getattr(args, "transport_used", args.transport),
                    "nnz_total": int(nnz_all), "ghosts_rank0": info["nghost"],
                    "l2": "inputs larger than L2 on every GPU"},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu_alg, 1), "peak": hbm, "peak_source": peak_src,
@@ -478,6 +492,7 @@ def run_cg_dist(args, rank, world, local):
         "config": {"workload": f"row-partitioned Jacobi PCG {iters} it, elasticity box slab of 87 node layers per "
                                f"GPU ({nloc} rows/GPU, natural ordering)", "config": "c5-weak",
                    "iterations_per_step": iters, "nrows_total": int(n_all), "nnz_total": int(nnz_all),
+                   "transport": getattr(args, "transport_used", args.transport),
                    "final_residual": float(res.residual_history[-1])},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(per_gpu / hbm, 4), "traffic": None,
@@ -775,6 +790,8 @@ def main():
     p.add_argument("--kernel", default=None)
     p.add_argument("--threshold", type=int, default=0)
     p.add_argument("--permuted", action="store_true")
+    p.add_argument("--transport", choices=["ipc", "nccl"], default="ipc",
+                   help="multi-GPU halo / dot transport (N > 1)")
     p.add_argument("--row-order", choices=["reference", "locality"], default=None,
                    help="r/rs kernels: reference sort_rows_desc order or the locality (Cuthill-McKee) order")
     p.add_argument("--scale", type=float, default=1.0, help="mesh edge scale (tests only)")

@@ -313,6 +313,28 @@ ew_status ew_dist_create_block(int64_t nrows_global, int64_t nrows_local, const 
                                const void* nccl_id, const char* kernel_id,
                                const ew_warp_config* cfg, const ew_kernel_options* opts,
                                void* stream, ew_dist* out);
+/* Peer transport, every partition in this process on the current device:
+ * the same push / mailbox kernels as the IPC transport, peers being the
+ * process's own partitions (tests the NVLink protocol on one GPU). */
+ew_status ew_dist_create_peer(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets,
+                              int64_t nnz, const int64_t* col_indices, const double* values,
+                              const int64_t* bounds, int32_t nparts, const char* kernel_id,
+                              const ew_warp_config* cfg, const ew_kernel_options* opts, void* stream,
+                              ew_dist* out);
+/* Rank-ordered allgather supplied by the caller (e.g. torch.distributed):
+ * recv receives world_size * bytes, rank g's send at offset g * bytes.
+ * Returns 0 on success. */
+typedef int (*ew_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
+/* One partition per process, peers reached through CUDA IPC mappings of each
+ * other's ghost buffers and mailboxes (NVLink stores; no NCCL on the data
+ * path). Same arguments as ew_dist_create_block, with the allgather used for
+ * setup (ghost requests, IPC handles). Collective: every rank calls it, and
+ * every rank destroys its operator only after the last solve on all ranks. */
+ew_status ew_dist_create_block_ipc(int64_t nrows_global, int64_t nrows_local, const int64_t* row_offsets,
+                                   const int64_t* col_indices, const double* values, const int64_t* bounds,
+                                   int32_t nparts, int32_t rank, ew_allgather_fn allgather, void* user,
+                                   const char* kernel_id, const ew_warp_config* cfg,
+                                   const ew_kernel_options* opts, void* stream, ew_dist* out);
 ew_status ew_dist_destroy(ew_dist d);
 /* Row range, ghost count and send count of local partition i. */
 ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* row_begin, int64_t* row_end,

@@ -164,6 +164,12 @@ _SIGS = {
     "ew_dist_create_block": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp,
                                        C.c_char_p, C.POINTER(WarpConfig), C.POINTER(KernelOptions), _vp,
                                        C.POINTER(_vp)]),
+    "ew_dist_create_peer": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, _vp, C.c_int32,
+                                      C.c_char_p, C.POINTER(WarpConfig), C.POINTER(KernelOptions), _vp,
+                                      C.POINTER(_vp)]),
+    "ew_dist_create_block_ipc": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32, C.c_int32,
+                                           _vp, _vp, C.c_char_p, C.POINTER(WarpConfig),
+                                           C.POINTER(KernelOptions), _vp, C.POINTER(_vp)]),
     "ew_dist_destroy": (C.c_int, [_vp]),
     "ew_dist_get_info": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, _i64p]),
     "ew_dist_spmv": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
@@ -644,6 +650,20 @@ def nccl_unique_id():
     return bytes(buf)
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+def torch_allgather(data: bytes):
+    """Rank-ordered allgather of a byte string over torch.distributed."""
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized():
+        return [data]  # a single process
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, data)
+    return out
+
+
 class Dist:
     """Row-partitioned operator + CG (ew_dist).
 
@@ -685,8 +705,59 @@ class Dist:
         return Dist(h)
 
     @staticmethod
-    def local(m, nparts, kernel="k1", bounds=None, warp_size=32, threshold=0, stream=None):
-        return Dist._make(m, nparts, 0, nparts, None, kernel, bounds, warp_size, threshold, stream)
+    def local(m, nparts, kernel="k1", bounds=None, warp_size=32, threshold=0, stream=None, transport="copy"):
+        """transport "copy": halos as device copies; "peer": the IPC
+        transport's push / mailbox kernels with this process's partitions as
+        the peers (ew_dist_create_peer)."""
+        if transport == "copy":
+            return Dist._make(m, nparts, 0, nparts, None, kernel, bounds, warp_size, threshold, stream)
+        if transport != "peer":
+            raise ValueError(f"unknown transport {transport!r}")
+        ro, ci, v = (_host(m.row_offsets, np.int64), _host(m.col_indices, np.int64), _host(m.values, np.float64))
+        b = _host(bounds, np.int64) if bounds is not None else None
+        cfg = WarpConfig.make(warp_size)
+        opts = KernelOptions(int(threshold), -1, 0)
+        h = C.c_void_p()
+        check(lib().ew_dist_create_peer(m.nrows, m.ncols, ro.size, _ptr(ro), ci.size, _ptr(ci), _ptr(v), _ptr(b),
+                                        int(nparts), kernel.encode(), C.byref(cfg), C.byref(opts),
+                                        _stream_ptr(stream), C.byref(h)))
+        return Dist(h)
+
+    @staticmethod
+    def block_ipc(nglobal, ro, ci, v, bounds, rank, allgather=None, kernel="k1", warp_size=32, threshold=0,
+                  stream=None):
+        """One partition per process over CUDA IPC (ew_dist_create_block_ipc).
+        allgather(bytes) -> list of bytes in rank order; default:
+        torch.distributed.all_gather_object on the default group."""
+        ro, ci, v = _host(ro, np.int64), _host(ci, np.int64), _host(v, np.float64)
+        b = _host(bounds, np.int64)
+        cfg = WarpConfig.make(warp_size)
+        opts = KernelOptions(int(threshold), -1, 0)
+        fn = allgather or torch_allgather
+        err = []
+
+        def cb(send, recv, nbytes, user):
+            try:
+                parts = fn(C.string_at(send, nbytes))
+                buf = b"".join(parts)
+                if len(buf) != nbytes * (b.size - 1):
+                    raise ValueError("allgather returned the wrong size")
+                C.memmove(recv, buf, len(buf))
+                return 0
+            except Exception as e:  # reported through the status code
+                err.append(e)
+                return 1
+
+        cfn = ALLGATHER_FN(cb)
+        h = C.c_void_p()
+        st = lib().ew_dist_create_block_ipc(int(nglobal), ro.size - 1, _ptr(ro), _ptr(ci), _ptr(v), _ptr(b),
+                                            b.size - 1, int(rank), C.cast(cfn, C.c_void_p), None,
+                                            kernel.encode(), C.byref(cfg), C.byref(opts), _stream_ptr(stream),
+                                            C.byref(h))
+        if err:
+            raise err[0]
+        check(st)
+        return Dist(h)
 
     @staticmethod
     def nccl(m, nparts, rank, nccl_id, kernel="k1", bounds=None, warp_size=32, threshold=0, stream=None):

@@ -662,6 +662,42 @@ ew_status ew_dist_create_block(int64_t nrows_global, int64_t nrows_local, const 
     });
 }
 
+ew_status ew_dist_create_peer(int64_t nrows, int64_t ncols, int64_t n_row_offsets, const int64_t* row_offsets,
+                              int64_t nnz, const int64_t* col_indices, const double* values, const int64_t* bounds,
+                              int32_t nparts, const char* kernel_id, const ew_warp_config* cfg,
+                              const ew_kernel_options* opts, void* stream, ew_dist* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && row_offsets != nullptr && kernel_id != nullptr, "null argument");
+        ew::require(n_row_offsets == nrows + 1 && row_offsets[nrows] == nnz, "row_offsets length");
+        if (nrows > 0x7fffffff) throw ew::Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        auto d = ew::dist_create(nrows, ncols, row_offsets, col_indices, values, bounds, nparts, 0, nparts, nullptr,
+                                 kernel_id, c, o, ew::as_stream(stream), /*peer=*/true);
+        *out = new ew_dist_t{std::move(d)};
+    });
+}
+
+ew_status ew_dist_create_block_ipc(int64_t nrows_global, int64_t nrows_local, const int64_t* row_offsets,
+                                   const int64_t* col_indices, const double* values, const int64_t* bounds,
+                                   int32_t nparts, int32_t rank, ew_allgather_fn allgather, void* user,
+                                   const char* kernel_id, const ew_warp_config* cfg, const ew_kernel_options* opts,
+                                   void* stream, ew_dist* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && row_offsets != nullptr && bounds != nullptr && kernel_id != nullptr,
+                    "null argument");
+        ew::require(rank >= 0 && rank < nparts && bounds[rank + 1] - bounds[rank] == nrows_local,
+                    "block rows do not match the partition bounds");
+        ew::require(row_offsets[0] == 0, "row_offsets[0] != 0");
+        if (nrows_global > 0x7fffffff) throw ew::Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        auto d = ew::dist_create_block_ipc(nrows_global, row_offsets, col_indices, values, bounds, nparts, rank,
+                                           allgather, user, kernel_id, c, o, ew::as_stream(stream));
+        *out = new ew_dist_t{std::move(d)};
+    });
+}
+
 ew_status ew_dist_destroy(ew_dist d) {
     return guarded([&] { delete d; });
 }

@@ -12,11 +12,20 @@
 // reduction: each partition's totals are all-gathered and summed in rank
 // order on every rank (deterministic, identical decisions everywhere).
 //
-// Transports: NCCL (one process per GPU; ncclSend/Recv inside a group and
-// ncclAllGather on the caller's stream; libnccl is resolved at run time, so
-// the process uses the same NCCL torch.distributed loaded) and an
-// in-process transport that runs all partitions on the current device with
-// device-to-device copies (tests the whole partitioned algorithm on 1 GPU).
+// Transports:
+//  * peer (one process per GPU, CUDA IPC): every rank maps its peers' ghost
+//    buffers and mailboxes; one push kernel gathers the owned values peers
+//    need and stores them straight into the peers' ghost tails over NVLink,
+//    then raises a flag in each peer's mailbox; dot products are published
+//    into every peer's mailbox and summed in rank order. No NCCL on the data
+//    path; setup data (ghost requests, IPC handles) goes through the
+//    caller's allgather callback. The same kernels run in-process with G
+//    partitions on one device (EW_TRANSPORT_PEER with ew_dist_create_peer).
+//  * NCCL (one process per GPU; ncclSend/Recv inside a group and
+//    ncclAllGather on the caller's stream; libnccl is resolved at run time, so
+//    the process uses the same NCCL torch.distributed loaded);
+//  * copy: all partitions in this process on the current device, halos as
+//    device-to-device copies (tests the partitioned algorithm on 1 GPU).
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -104,6 +113,26 @@ std::vector<int64_t> partition_rows(const int64_t* ro, int64_t nrows, int32_t np
     return b;
 }
 
+// A destination of the peer push: send_idx[off, off + cnt) go to the ghost
+// tail segment dst_p / dst_x (the peer's p_ext / x_ext) of partition `peer`.
+struct PushDesc {
+    int64_t off, cnt;
+    double* dst_p;
+    double* dst_x;
+    int32_t peer;
+};
+
+// Mailbox words of a partition in a G-way peer transport.
+struct Mbox {
+    __host__ __device__ static size_t words(int32_t G) { return 7 * static_cast<size_t>(G); }
+    __host__ __device__ static size_t halo(int32_t g) { return g; }                       // halo epoch raised by g
+    __host__ __device__ static size_t ack(int32_t G, int32_t g) { return G + g; }         // g consumed this rank's epoch
+    __host__ __device__ static size_t red(int32_t G, int32_t g) { return 2 * G + g; }     // reduction epoch raised by g
+    __host__ __device__ static size_t val(int32_t G, int32_t g, uint64_t e) {             // 2 doubles, parity buffered
+        return 3 * G + ((e & 1) * G + g) * 2;
+    }
+};
+
 struct DistPart {
     int32_t part = 0;
     int64_t r0 = 0, r1 = 0, nloc = 0, nghost = 0;
@@ -122,6 +151,13 @@ struct DistPart {
     DevBuf<double> x_ext, p_ext, r, q, b, diag, hist, partials, gathered;
     DevBuf<unsigned> tickets;  // SpMV-fused p.q grid sum (cg::grid_sum)
     DevBuf<cg::State> st;
+    // peer transport: mailbox (flags + published dot products), push plan
+    DevBuf<uint64_t> mbox;
+    DevBuf<unsigned> push_ctr;
+    DevBuf<PushDesc> descs;  // one per destination peer
+    DevBuf<int32_t> srcs;    // peers that send to this partition
+    DevBuf<uint64_t*> mboxes;  // every partition's mailbox, by partition index
+    int32_t ndesc = 0, nsrc = 0;
 };
 
 struct DistData {
@@ -129,12 +165,17 @@ struct DistData {
     std::vector<int64_t> bounds;
     std::vector<std::unique_ptr<DistPart>> parts;  // this process's partitions
     bool use_nccl = false;
+    bool peer = false;                     // peer transport (in-process or CUDA IPC)
+    bool ipc = false;                      // peers live in other processes
+    uint64_t halo_epoch = 0, red_epoch = 0;
+    std::vector<void*> ipc_mapped;         // cudaIpcOpenMemHandle mappings to close
     ncclComm_t comm = nullptr;
     std::string kernel_id;
     bool split = false;                    // every part has op_int / op_bnd
     cudaStream_t comm_stream = nullptr;    // halo exchange, concurrent with the interior rows
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ~DistData() {
+        for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
         if (ev_ready) cudaEventDestroy(ev_ready);
         if (ev_halo) cudaEventDestroy(ev_halo);
         if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -143,6 +184,96 @@ struct DistData {
 };
 
 namespace {
+
+// ---- peer transport kernels --------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t e) {
+    while (ld_acquire_sys(p) < e) __nanosleep(64);
+}
+
+// Pack and transfer in one kernel: the owned values each destination needs
+// are stored straight into its ghost tail (peer stores over NVLink), then the
+// last CTA raises the destination's halo flag (release, system scope).
+// Before writing, every destination must have consumed the previous epoch
+// (its ack in this rank's mailbox); with write_acks this rank first acks the
+// previous epoch to its own sources (its boundary rows of that epoch are
+// done: this kernel is stream-ordered after them).
+__global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int32_t* __restrict__ idx,
+                            const double* __restrict__ src, int which, uint64_t epoch, uint64_t* const* mboxes,
+                            int me, int G, int write_acks, const int32_t* __restrict__ srcs, int nsrc,
+                            unsigned* ctr, int64_t total) {
+    uint64_t* mine = mboxes[me];
+    if (write_acks && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch - 1);
+    for (int i = threadIdx.x; i < ndesc; i += blockDim.x) spin_until(mine + Mbox::ack(G, d[i].peer), epoch - 1);
+    __syncthreads();
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+        int i = 0;
+        while (k >= d[i].off + d[i].cnt) ++i;
+        double* dst = (which ? d[i].dst_x : d[i].dst_p) + (k - d[i].off);
+        *dst = src[idx[k]];
+    }
+    __threadfence_system();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence_system();
+    for (int i = threadIdx.x; i < ndesc; i += blockDim.x) st_release_sys(mboxes[d[i].peer] + Mbox::halo(me), epoch);
+    if (threadIdx.x == 0) *ctr = 0;
+}
+
+// In-process peer transport: acks as their own launch (every partition's
+// boundary rows precede every push on the one device).
+__global__ void ack_kernel(uint64_t* const* mboxes, int me, int G, const int32_t* __restrict__ srcs, int nsrc,
+                           uint64_t epoch) {
+    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch);
+}
+
+// The ghost tail is complete once every source raised this epoch.
+__global__ void halo_wait_kernel(const uint64_t* mine, const int32_t* __restrict__ srcs, int nsrc, uint64_t epoch) {
+    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) spin_until(mine + Mbox::halo(srcs[i]), epoch);
+}
+
+// Reduction, step 1: this partition's totals (State::loc) into slot `me` of
+// every partition's mailbox (its own included), then the flag.
+__global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int me, int G, uint64_t epoch) {
+    const int g = threadIdx.x;
+    if (g >= G) return;
+    uint64_t* mb = mboxes[g];
+    double* v = reinterpret_cast<double*>(mb + Mbox::val(G, me, epoch));
+    v[0] = st->loc[0];
+    v[1] = st->loc[1];
+    __threadfence_system();
+    st_release_sys(mb + Mbox::red(G, me), epoch);
+}
+
+// Reduction, step 2: wait for every partition's totals, copy them to
+// `gathered` in rank order (then cg::finalize_kernel sums them).
+__global__ void collect_kernel(const uint64_t* mine, int G, uint64_t epoch, double* gathered) {
+    const int g = threadIdx.x;
+    if (g >= G) return;
+    spin_until(mine + Mbox::red(G, g), epoch);
+    const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
+    gathered[2 * g] = ld_relaxed_sys(v);
+    gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
+}
 
 // Ghost columns of a row block [r0, r1) given with global column ids:
 // sorted, unique, every column outside the block.
@@ -259,10 +390,48 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+// Peer transport, first half: push this epoch's values into the peers'
+// ghost tails (on stream s). which: 0 p_ext, 1 x_ext.
+void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+    const uint64_t e = ++D.halo_epoch;
+    const int32_t G = D.nparts;
+    if (!D.ipc) {
+        for (auto& P : D.parts) {
+            if (!P->nsrc) continue;
+            ack_kernel<<<1, 32, 0, s>>>(P->mboxes.get(), P->part, G, P->srcs.get(), P->nsrc, e - 1);
+            launched("ack_kernel");
+        }
+    }
+    for (auto& P : D.parts) {
+        const int64_t total = static_cast<int64_t>(P->send_idx.size());
+        if (!total && (!D.ipc || !P->nsrc)) continue;
+        const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(total), 148 * 4));
+        push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), ((*P).*ext).get(), which, e,
+                                            P->mboxes.get(), P->part, G, D.ipc ? 1 : 0, P->srcs.get(), P->nsrc,
+                                            P->push_ctr.get(), total);
+        launched("push_kernel");
+    }
+}
+
+// Peer transport, second half: on stream s, wait until every ghost of this
+// epoch has landed.
+void peer_wait(DistData& D, cudaStream_t s) {
+    for (auto& P : D.parts) {
+        if (!P->nsrc) continue;
+        halo_wait_kernel<<<1, 32, 0, s>>>(P->mbox.get(), P->srcs.get(), P->nsrc, D.halo_epoch);
+        launched("halo_wait_kernel");
+    }
+}
+
 // Exchange the owned values peers need into every partition's ghost tail.
 void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
     const int32_t G = D.nparts;
     if (G == 1) return;
+    if (D.peer) {
+        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, s);
+        peer_wait(D, s);
+        return;
+    }
     for (auto& P : D.parts) {
         const int64_t ns = static_cast<int64_t>(P->send_idx.size());
         if (ns) {
@@ -301,6 +470,18 @@ void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
 
 // Every partition's State::loc[0..1] into every partition's `gathered`.
 void allgather(DistData& D, cudaStream_t s) {
+    if (D.peer) {
+        const uint64_t e = ++D.red_epoch;
+        for (auto& P : D.parts) {
+            publish_kernel<<<1, 32, 0, s>>>(P->st.get(), P->mboxes.get(), P->part, D.nparts, e);
+            launched("publish_kernel");
+        }
+        for (auto& P : D.parts) {
+            collect_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, e, P->gathered.get());
+            launched("collect_kernel");
+        }
+        return;
+    }
     if (D.use_nccl) {
         DistPart& P = *D.parts[0];
         nccl_check(nccl().AllGather(P.st.get()->loc, P.gathered.get(), 2, ncclFloat64, D.comm, s), "ncclAllGather");
@@ -324,11 +505,23 @@ void finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaS
 void halo_begin(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
     EW_CUDA_CHECK(cudaEventRecord(D.ev_ready, s));
     EW_CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_ready, 0));
+    if (D.peer) {  // the push runs beside the interior rows; peer_wait orders the boundary rows
+        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, D.comm_stream);
+        return;
+    }
     halo(D, ext, D.comm_stream);
     EW_CUDA_CHECK(cudaEventRecord(D.ev_halo, D.comm_stream));
 }
 
-void halo_end(DistData& D, cudaStream_t s) { EW_CUDA_CHECK(cudaStreamWaitEvent(s, D.ev_halo, 0)); }
+void halo_end(DistData& D, cudaStream_t s) {
+    if (D.peer) {
+        peer_wait(D, s);
+        // the push kernels read p_ext / x_ext: the next writer (p update) on s
+        // must not overtake them
+        EW_CUDA_CHECK(cudaEventRecord(D.ev_halo, D.comm_stream));
+    }
+    EW_CUDA_CHECK(cudaStreamWaitEvent(s, D.ev_halo, 0));
+}
 
 // One row set of a split part; with `dot`, its p.q partial goes to loc[slot].
 // False when the fused dot was not available (the caller runs pq_kernel).
@@ -380,6 +573,60 @@ void spmv_exchange(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, b
     }
 }
 
+// Peer plan of partition P: its mailbox, sources, and one push descriptor
+// per destination h (the ghost segment h keeps for P's values starts at
+// h's nloc + h's recv_off[P]). peer_p/x/mbox/nloc/recv index partitions.
+void peer_plan(DistPart& P, int32_t G, const std::vector<double*>& peer_p, const std::vector<double*>& peer_x,
+               const std::vector<uint64_t*>& mbox, const std::vector<int64_t>& tail_off, cudaStream_t s) {
+    std::vector<PushDesc> d;
+    for (int32_t h = 0; h < G; ++h) {
+        const int64_t cnt = P.send_off[h + 1] - P.send_off[h];
+        if (h == P.part || !cnt) continue;
+        d.push_back(PushDesc{P.send_off[h], cnt, peer_p[h] + tail_off[h], peer_x[h] + tail_off[h], h});
+    }
+    std::vector<int32_t> src;
+    for (int32_t h = 0; h < G; ++h)
+        if (h != P.part && P.recv_off[h + 1] > P.recv_off[h]) src.push_back(h);
+    P.ndesc = static_cast<int32_t>(d.size());
+    P.nsrc = static_cast<int32_t>(src.size());
+    P.descs.alloc(std::max<size_t>(1, d.size()));
+    P.srcs.alloc(std::max<size_t>(1, src.size()));
+    P.mboxes.alloc(G);
+    if (!d.empty())
+        EW_CUDA_CHECK(cudaMemcpyAsync(P.descs.get(), d.data(), d.size() * sizeof(PushDesc), cudaMemcpyHostToDevice, s));
+    if (!src.empty())
+        EW_CUDA_CHECK(cudaMemcpyAsync(P.srcs.get(), src.data(), src.size() * 4, cudaMemcpyHostToDevice, s));
+    EW_CUDA_CHECK(cudaMemcpyAsync(P.mboxes.get(), mbox.data(), G * sizeof(uint64_t*), cudaMemcpyHostToDevice, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void alloc_mailbox(DistPart& P, int32_t G, cudaStream_t s) {
+    P.mbox.alloc(Mbox::words(G));
+    P.push_ctr.alloc(1);
+    EW_CUDA_CHECK(cudaMemsetAsync(P.mbox.get(), 0, P.mbox.bytes(), s));
+    EW_CUDA_CHECK(cudaMemsetAsync(P.push_ctr.get(), 0, P.push_ctr.bytes(), s));
+}
+
+// In-process peer transport: the "peers" are this process's partitions.
+void peer_setup_local(DistData& D, cudaStream_t s) {
+    const int32_t G = D.nparts;
+    for (auto& P : D.parts) alloc_mailbox(*P, G, s);
+    std::vector<double*> pp(G), px(G);
+    std::vector<uint64_t*> mb(G);
+    for (auto& P : D.parts) {
+        pp[P->part] = P->p_ext.get();
+        px[P->part] = P->x_ext.get();
+        mb[P->part] = P->mbox.get();
+    }
+    for (auto& P : D.parts) {
+        std::vector<int64_t> tail(G, 0);
+        for (auto& H : D.parts)
+            if (H->part != P->part) tail[H->part] = H->nloc + H->recv_off[P->part];
+        peer_plan(*P, G, pp, px, mb, tail, s);
+    }
+    D.peer = true;
+}
+
 void init_overlap(DistData& D) {
     D.split = !D.parts.empty();
     for (auto& P : D.parts) D.split = D.split && P->op_int && P->op_bnd;
@@ -394,7 +641,8 @@ void init_overlap(DistData& D) {
 std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
                                       const double* v, const int64_t* bounds_in, int32_t nparts, int32_t first,
                                       int32_t nlocal, const void* nccl_id, const std::string& kid,
-                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s) {
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s,
+                                      bool peer) {
     require(nrows == ncols, "partitioned operator must be square");
     require(nparts >= 1 && first >= 0 && nlocal >= 1 && first + nlocal <= nparts, "bad partition range");
     require(kid == "k1" || kid == "k2" || kid == "csr_ref" || kid == "csr_vector" || kid == "ell" || kid == "hyb" ||
@@ -431,6 +679,10 @@ std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_
         auto P = std::make_unique<DistPart>();
         build_part(*P, g, nparts, D->bounds, ro + D->bounds[g], ci, v, ghosts[g], needs, kid, cfg, opts, s);
         D->parts.push_back(std::move(P));
+    }
+    if (peer) {
+        require(!D->use_nccl, "the in-process peer transport holds every partition");
+        if (nparts > 1) peer_setup_local(*D, s);
     }
     init_overlap(*D);
     return D;
@@ -500,6 +752,100 @@ std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro,
     }
     auto P = std::make_unique<DistPart>();
     build_part(*P, rank, nparts, D->bounds, bro, bci, bv, ghosts, needs, kid, cfg, opts, s);
+    D->parts.push_back(std::move(P));
+    init_overlap(*D);
+    return D;
+}
+
+std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* bro, const int64_t* bci,
+                                                const double* bv, const int64_t* bounds, int32_t nparts,
+                                                int32_t rank, ew_allgather_fn allgather, void* user,
+                                                const std::string& kid, const ew_warp_config& cfg,
+                                                const ew_kernel_options& opts, cudaStream_t s) {
+    require(allgather != nullptr, "the IPC transport needs an allgather callback");
+    require(nparts >= 1 && rank >= 0 && rank < nparts, "bad rank");
+    require(kid == "k1" || kid == "k2" || kid == "csr_ref",
+            "partitioned kernels: k1, k2 or csr_ref (the local matrix has ghost columns)");
+    auto D = std::make_shared<DistData>();
+    D->nparts = nparts;
+    D->first = rank;
+    D->nlocal = 1;
+    D->kernel_id = kid;
+    D->bounds.assign(bounds, bounds + nparts + 1);
+    require(D->bounds.front() == 0 && D->bounds.back() == nglobal, "partition bounds must cover [0, nrows]");
+    for (int32_t g = 0; g < nparts; ++g) require(D->bounds[g] <= D->bounds[g + 1], "partition bounds must be sorted");
+    const int32_t G = nparts;
+    auto ag = [&](const void* send, void* recv, size_t bytes) {
+        if (allgather(send, recv, bytes, user) != 0) throw Error(EW_INVALID_ARGUMENT, "allgather callback failed");
+    };
+    const int64_t r0 = D->bounds[rank], r1 = D->bounds[rank + 1];
+    const std::vector<int64_t> ghosts = ghost_list(bro, bci, r0, r1);
+    // ghost requests: counts per owner, then the (owner-grouped, ascending) ids
+    std::vector<int64_t> my_need(G, 0), all(static_cast<size_t>(G) * G);
+    for (int64_t c : ghosts) my_need[owner_of(D->bounds, c)]++;
+    ag(my_need.data(), all.data(), G * sizeof(int64_t));
+    int64_t maxg = 1;
+    for (int32_t h = 0; h < G; ++h) {
+        int64_t t = 0;
+        for (int32_t g = 0; g < G; ++g) t += all[static_cast<size_t>(h) * G + g];
+        maxg = std::max(maxg, t);
+    }
+    std::vector<int64_t> mine(maxg, -1), every(static_cast<size_t>(G) * maxg);
+    std::copy(ghosts.begin(), ghosts.end(), mine.begin());
+    ag(mine.data(), every.data(), maxg * sizeof(int64_t));
+    auto before = [&](int32_t h, int32_t owner) {  // h's ghosts owned by ranks < owner
+        int64_t t = 0;
+        for (int32_t g = 0; g < owner; ++g) t += all[static_cast<size_t>(h) * G + g];
+        return t;
+    };
+    std::vector<std::vector<int64_t>> needs(G);
+    for (int32_t h = 0; h < G; ++h) {
+        if (h == rank) continue;
+        const int64_t* lst = every.data() + static_cast<size_t>(h) * maxg + before(h, rank);
+        needs[h].assign(lst, lst + all[static_cast<size_t>(h) * G + rank]);
+    }
+    auto P = std::make_unique<DistPart>();
+    build_part(*P, rank, nparts, D->bounds, bro, bci, bv, ghosts, needs, kid, cfg, opts, s);
+    if (G > 1) {
+        require(P->nloc > 0, "the IPC transport needs at least one row per rank");
+        alloc_mailbox(*P, G, s);
+        struct Ex {
+            cudaIpcMemHandle_t p, x, mb;
+        } ex{}, *exs = nullptr;
+        EW_CUDA_CHECK(cudaIpcGetMemHandle(&ex.p, P->p_ext.get()));
+        EW_CUDA_CHECK(cudaIpcGetMemHandle(&ex.x, P->x_ext.get()));
+        EW_CUDA_CHECK(cudaIpcGetMemHandle(&ex.mb, P->mbox.get()));
+        std::vector<Ex> all_ex(G);
+        exs = all_ex.data();
+        ag(&ex, exs, sizeof(Ex));
+        std::vector<double*> pp(G), px(G);
+        std::vector<uint64_t*> mb(G);
+        std::vector<int64_t> tail(G, 0);
+        for (int32_t h = 0; h < G; ++h) {
+            if (h == rank) {
+                pp[h] = P->p_ext.get();
+                px[h] = P->x_ext.get();
+                mb[h] = P->mbox.get();
+                continue;
+            }
+            void* ptr = nullptr;
+            for (auto [handle, slot] : {std::pair{&exs[h].p, 0}, std::pair{&exs[h].x, 1}, std::pair{&exs[h].mb, 2}}) {
+                EW_CUDA_CHECK(cudaIpcOpenMemHandle(&ptr, *handle, cudaIpcMemLazyEnablePeerAccess));
+                D->ipc_mapped.push_back(ptr);
+                if (slot == 0) pp[h] = static_cast<double*>(ptr);
+                if (slot == 1) px[h] = static_cast<double*>(ptr);
+                if (slot == 2) mb[h] = static_cast<uint64_t*>(ptr);
+            }
+            tail[h] = (D->bounds[h + 1] - D->bounds[h]) + before(h, rank);
+        }
+        peer_plan(*P, G, pp, px, mb, tail, s);
+        D->peer = D->ipc = true;
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        int64_t token = rank, tokens_out[1];
+        std::vector<int64_t> tokens(G);
+        (void)tokens_out;
+        ag(&token, tokens.data(), sizeof(token));  // every mailbox zeroed and mapped before any push
+    }
     D->parts.push_back(std::move(P));
     init_overlap(*D);
     return D;
@@ -583,7 +929,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         if (h.status == cg::kBadRhs) flags[0] = 1.0;
         if (h.flags & 2) flags[1] = 1.0;
     }
-    if (D.use_nccl) {  // share the flags: all ranks take the same branch
+    if (D.use_nccl || D.ipc) {  // share the flags: all ranks take the same branch
         DistPart& P = *D.parts[0];
         EW_CUDA_CHECK(cudaMemcpyAsync(P.st.get()->loc, flags, 16, cudaMemcpyHostToDevice, s));
         allgather(D, s);

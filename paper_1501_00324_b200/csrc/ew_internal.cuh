@@ -327,7 +327,15 @@ std::vector<int64_t> partition_rows(const int64_t* ro, int64_t nrows, int32_t np
 std::shared_ptr<DistData> dist_create(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
                                       const double* v, const int64_t* bounds, int32_t nparts, int32_t first,
                                       int32_t nlocal, const void* nccl_id, const std::string& kid,
-                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s);
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s,
+                                      bool peer = false);
+// One partition per process over CUDA IPC (peer transport); setup data goes
+// through the caller's allgather (ew_allgather_fn).
+std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* bro, const int64_t* bci,
+                                                const double* bv, const int64_t* bounds, int32_t nparts,
+                                                int32_t rank, ew_allgather_fn allgather, void* user,
+                                                const std::string& kid, const ew_warp_config& cfg,
+                                                const ew_kernel_options& opts, cudaStream_t s);
 std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro, const int64_t* bci,
                                             const double* bv, const int64_t* bounds, int32_t nparts, int32_t rank,
                                             const void* nccl_id, const std::string& kid, const ew_warp_config& cfg,

@@ -48,15 +48,19 @@ def test_partition_rule(ew, fem):
         assert b[g] == 0 or fem.row_offsets[b[g] - 1] < g * nnz // 4
 
 
+@pytest.mark.parametrize("transport", ["copy", "peer"])
 @pytest.mark.parametrize("nparts", [1, 2, 3, 5])
 @pytest.mark.parametrize("kernel", ["k1", "k2", "csr_ref"])
-def test_partitioned_spmv_matches_single_gpu(ew, R, fem, nparts, kernel):
+def test_partitioned_spmv_matches_single_gpu(ew, R, fem, nparts, kernel, transport):
     x = np.random.default_rng(nparts).uniform(0.1, 1.0, fem.ncols)
     a = ew.Csr(fem.nrows, fem.ncols, fem.row_offsets, fem.col_indices, fem.values)
     single = ew.Kernel(kernel, a, threshold=4).apply(x)
-    d = ew.Dist.local(fem, nparts, kernel=kernel, threshold=4)
+    d = ew.Dist.local(fem, nparts, kernel=kernel, threshold=4, transport=transport)
     assert d.owned == fem.nrows and d.nlocal == nparts
     y = d.spmv(x)
+    for _ in range(3):  # back-to-back exchanges: the peer transport's acks
+        y2 = d.spmv(x)
+        assert np.array_equal(bits(y2), bits(y))
     if kernel == "k2":
         # a K2 row's chunk length is the max over the rows sharing its warp
         # (warp_layout.cpp:108-112), and partitioning regroups warps: the
@@ -76,12 +80,13 @@ def spd(F):
     return F.fem_tet_graph(3000, 5, 21, 12)
 
 
+@pytest.mark.parametrize("transport", ["copy", "peer"])
 @pytest.mark.parametrize("nparts", [1, 2, 4])
-def test_partitioned_cg_matches_reference(ew, R, spd, nparts):
+def test_partitioned_cg_matches_reference(ew, R, spd, nparts, transport):
     b = R.spmv_csr(spd, np.ones(spd.ncols))
     diag = R.extract_diagonal(spd)
     ref = R.cg_csr(spd, b)
-    d = ew.Dist.local(spd, nparts)
+    d = ew.Dist.local(spd, nparts, transport=transport)
     res = d.cg_solve(b, diag)
     assert res.converged and res.iterations == ref.iterations and res.spmv_calls == ref.spmv_calls
     assert hist_ok(res.residual_history, ref.residual_history)
@@ -105,12 +110,13 @@ def test_partitioned_cg_ill_conditioned_fem(ew, R, fem):
     assert drift_one < 1e-6 and drift_part < 1e-6
 
 
-def test_partitioned_cg_long_run_and_errors(ew, R, spd):
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_partitioned_cg_long_run_and_errors(ew, R, spd, transport):
     rng = np.random.default_rng(3)
     b = rng.uniform(-1, 1, spd.nrows)
     diag = R.extract_diagonal(spd)
     ref = R.cg_csr(spd, b, tol=1e-300, max_iterations=120, recompute=7)
-    d = ew.Dist.local(spd, 3)
+    d = ew.Dist.local(spd, 3, transport=transport)
     res = d.cg_solve(b, diag, tol=1e-300, max_iterations=120, recompute_interval=7)
     assert res.iterations == 120 and not res.converged and res.spmv_calls == ref.spmv_calls
     assert hist_ok(res.residual_history, ref.residual_history)
@@ -157,3 +163,74 @@ def test_nccl_transport_one_rank(ew, R, fem):
     # one partition: same kernels, same reductions -> the single-GPU history
     assert res.iterations == one.iterations
     assert np.max(np.abs(res.residual_history - one.residual_history) / (1 + one.residual_history)) < 1e-6
+
+
+def _ipc_worker(rank, world, port, q):
+    """One rank of the IPC transport; both ranks share the one GPU (CUDA IPC
+    works between processes on the same device), so the push / mailbox
+    protocol runs across real process boundaries."""
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from oracle.oracle import Csr, Restatement
+        from paper_1501_00324_b200 import capi
+        from paper_1501_00324_b200 import workloads as W
+
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        n, _, ro, ci, v = W.elasticity_box(6, 5, 7)
+        m = Csr.make(n, n, ro, ci, v)
+        R = Restatement()
+        bounds = capi.partition_rows(ro, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        bro = ro[r0:r1 + 1] - ro[r0]
+        d = capi.Dist.block_ipc(n, bro, ci[ro[r0]:ro[r1]], v[ro[r0]:ro[r1]], bounds, rank)
+        x = np.random.default_rng(5).uniform(0.1, 1.0, n)
+        a = capi.Csr(n, n, ro, ci, v)
+        single = capi.Kernel("k1", a).apply(x)
+        ys = [d.spmv(x[r0:r1]) for _ in range(4)]
+        ok_spmv = all(same_up_to_zero_sign(y, single[r0:r1]) for y in ys)
+        sp = W.laplacian_box(9, 8, 7)
+        n2, _, ro2, ci2, v2 = sp
+        m2 = Csr.make(n2, n2, ro2, ci2, v2)
+        b2 = R.spmv_csr(m2, np.ones(n2))
+        ref = R.cg_csr(m2, b2)
+        bounds2 = capi.partition_rows(ro2, world)
+        s0, s1 = int(bounds2[rank]), int(bounds2[rank + 1])
+        d2 = capi.Dist.block_ipc(n2, ro2[s0:s1 + 1] - ro2[s0], ci2[ro2[s0]:ro2[s1]], v2[ro2[s0]:ro2[s1]], bounds2,
+                                 rank)
+        diag = R.extract_diagonal(m2)
+        res = d2.cg_solve(b2[s0:s1], diag[s0:s1])
+        ok_cg = (res.converged and res.iterations == ref.iterations and
+                 hist_ok(res.residual_history, ref.residual_history) and
+                 np.allclose(res.solution, ref.solution[s0:s1], rtol=1e-8, atol=1e-10))
+        dist.barrier()
+        del d, d2
+        dist.barrier()
+        q.put((rank, ok_spmv, ok_cg, res.iterations, ref.iterations))
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        q.put((rank, False, False, repr(e), None))
+
+
+def test_ipc_transport_two_processes(ew):
+    """Two processes, one partition each, over the CUDA IPC peer transport
+    (gloo only for the setup allgather)."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
+        assert ok_spmv, (rank, it)
+        assert ok_cg, (rank, it, ref_it)
