@@ -376,8 +376,8 @@ static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, c
 }
 
 // DIST: sum the all-gathered partition totals in rank order, then decide.
-static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, long long k, double tol,
-                                double divergence, State* st, double* hist) {
+__device__ __forceinline__ void finalize_body(int what, const double* gathered, int nparts, long long k, double tol,
+                                              double divergence, State* st, double* hist) {
     if (what != kBnorm && what != kStart && st->done) return;
     double t0 = 0.0, t1 = 0.0;
     for (int g = 0; g < nparts; ++g) {
@@ -390,6 +390,11 @@ static __global__ void finalize_kernel(int what, const double* __restrict__ gath
         case kPq: decide_pq(st, __dadd_rn(t0, t1)); break;  // interior + boundary row sets
         default: decide_update(st, t0, t1, k, tol, divergence, hist); break;
     }
+}
+
+static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, long long k,
+                                       double tol, double divergence, State* st, double* hist) {
+    finalize_body(what, gathered, nparts, k, tol, divergence, st, hist);
 }
 
 inline unsigned red_grid(int64_t n) {
