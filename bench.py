@@ -547,11 +547,36 @@ def run_cg(args, rank, world, local):
         "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
                    "row_order": args.row_order, "iterations_per_step": iters, "nrows": n, "nnz": nnz,
                    "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3)},
-        "roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
-                     "traffic": None, "algorithmic_bytes_per_iteration": b_it},
+        "roofline": None,
+        "iteration_roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
+                               "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
+                               "algorithmic_bytes_per_iteration": b_it,
+                               "note": "12 nnz + 104 n + refresh share per iteration / iteration time"},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    # dominant kernel: the SpMV (~2/3 of an iteration), timed alone with CUDA
+    # events on its stream, x (a CG direction) L2-resident as in the solve
+    stream = torch.cuda.current_stream()
+    xs = torch.tensor(np.random.default_rng(1).uniform(0.1, 1.0, nc), device="cuda")
+    ys = torch.empty(n, dtype=torch.float64, device="cuda")
+    spmv = k.apply_permuted if k.has_perm else k.apply
+    for _ in range(5):
+        spmv(xs, ys, stream=stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(50):
+        spmv(xs, ys, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    t_k = e0.elapsed_time(e1) * 1e-3 / 50
+    alg = 12 * nnz + 8 * n + 8 * nc
+    key = f"{args.config}/cg_k1_dot/{args.row_order}"
+    out["roofline"] = {"bound": "hbm", "achieved": round(alg / t_k / 1e9, 1), "peak": hbm, "peak_source": peak_src,
+                       "unit": "GB/s", "frac": round(alg / t_k / 1e9 / hbm, 4),
+                       "traffic": ncu_traffic(key) if args.scale == 1.0 else None,
+                       "traffic_source": f"profiles/ncu_traffic.json[{key}] (the CG's SpMV+p.q kernel)",
+                       "kernel": "k1_kernel", "kernel_us": round(t_k * 1e6, 2),
+                       "algorithmic_bytes_per_launch": alg}
     # end to end through ew_cg_solve[_permuted] with host b / diag / x
     bh = np.ascontiguousarray(b)
     t = time.perf_counter()

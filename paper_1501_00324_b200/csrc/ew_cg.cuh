@@ -32,6 +32,8 @@ struct State {
     double rz, pq, alpha, beta, bnorm, rr, rz_new;
     int done, status;
     long long iterations;
+    long long cur_it;     // iteration the reductions belong to (advanced by decide_pq)
+    long long max_it;     // CgConfig::max_iterations (set by the host before the solve)
     unsigned int ticket;  // last-CTA election counter
     int flags;            // bit 0: non-finite residual entry; bit 1: zero diagonal
     double loc[2];        // DIST: this partition's totals of the current reduction
@@ -164,6 +166,15 @@ __device__ __forceinline__ void decide_start(State* st, double rr, double rz, do
 }
 
 __device__ __forceinline__ void decide_pq(State* st, double pq) {
+    // a new iteration; past max_iterations the loop has ended (cg.cpp:69),
+    // not converged. Launches run ahead in whole blocks (CUDA graph) and
+    // become no-ops from here on.
+    const long long k = st->cur_it + 1;
+    if (k > st->max_it) {
+        st->done = 1;
+        return;
+    }
+    st->cur_it = k;
     st->pq = pq;  // cg.cpp:72-77
     if (!isfinite(pq) || pq <= 0.0) {
         st->status = kBreakdown;
@@ -173,8 +184,9 @@ __device__ __forceinline__ void decide_pq(State* st, double pq) {
     }
 }
 
-__device__ __forceinline__ void decide_update(State* st, double rr, double rz_new, long long k, double tol,
-                                              double divergence, double* hist) {
+__device__ __forceinline__ void decide_update(State* st, double rr, double rz_new, double tol, double divergence,
+                                              double* hist) {
+    const long long k = st->cur_it;
     st->rr = rr;
     st->rz_new = rz_new;
     // check_finite(r), cg.cpp:87. A non-finite entry makes r.r non-finite,
@@ -343,11 +355,14 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
     if (mode == 1) return;
     if (bad) atomicOr(&st->flags, 1);
     finish<DIST, 2>(v, partials, st, [&](const double (&t)[2]) {
-        decide_update(st, t[0], t[1], k, tol, divergence, hist);
+        decide_update(st, t[0], t[1], tol, divergence, hist);
     });
 }
 
 // p = z + beta p (cg.cpp:96-99)
+// Walks the vectors from the top down: the update kernel just walked them
+// bottom up, so the lines it touched last (r, diag, p of the top indices)
+// are the ones still in L2 when this kernel starts.
 static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, const double* __restrict__ r,
                                                 const double* __restrict__ diag, int64_t n, int jacobi,
                                                 const State* st) {
@@ -358,22 +373,52 @@ static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, c
         double rv[kU], dv[kU], pv[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int64_t i = i0 + u * S;
-            const bool ok = i < n;
+            const int64_t i = n - 1 - (i0 + u * S);
+            const bool ok = i >= 0;
             rv[u] = ok ? r[i] : 0.0;
             dv[u] = ok && jacobi ? diag[i] : 1.0;
             pv[u] = ok ? p[i] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int64_t i = i0 + u * S;
-            if (i >= n) continue;
+            const int64_t i = n - 1 - (i0 + u * S);
+            if (i < 0) continue;
             const double zi = jacobi ? __ddiv_rn(rv[u], dv[u]) : rv[u];
             p[i] = __dadd_rn(zi, __dmul_rn(beta, pv[u]));
         }
     }
     pdl_trigger();
 }
+
+// Ends the SpMV-fused p.q (ew_spmv.cu k1_dot_kernel writes one partial per
+// SpMV CTA and exits without a grid-level handshake): CTA f sums partials
+// [256 f, 256 f + 256) (one load per thread, fixed tree), then cg::grid_sum
+// over these CTAs in `scratch`; its last CTA decides alpha / breakdown, or
+// stores the partition total in loc[slot] for a partitioned solve.
+static __global__ void __launch_bounds__(kRedBlock) dot_final_kernel(const double* __restrict__ part, unsigned n,
+                                                                     double* scratch, unsigned* tickets, State* st,
+                                                                     int dist, int slot) {
+    pdl_wait();
+    if (st->done) return;  // uniform across the grid
+    const unsigned i = blockIdx.x * kRedBlock + threadIdx.x;
+    double v[1] = {i < n ? part[i] : 0.0};
+    block_sum<1>(v);
+    double total;
+    if (!grid_sum(v[0], scratch, tickets, &st->ticket, total)) return;
+    if (dist) {
+        st->loc[slot] = total;
+        if (slot == 0) st->loc[1] = 0.0;
+    } else {
+        decide_pq(st, total);
+    }
+}
+
+// partials / tickets the fused p.q of a plain SpMV grid of `blocks` CTAs needs
+inline size_t dot_final_blocks(int64_t blocks) { return static_cast<size_t>((blocks + kRedBlock - 1) / kRedBlock); }
+inline size_t dot_partials(int64_t blocks) {
+    return static_cast<size_t>(blocks) + grid_sum_partials(static_cast<int64_t>(dot_final_blocks(blocks)));
+}
+inline size_t dot_tickets(int64_t blocks) { return grid_sum_tickets(static_cast<int64_t>(dot_final_blocks(blocks))); }
 
 // DIST: sum the all-gathered partition totals in rank order, then decide.
 __device__ __forceinline__ void finalize_body(int what, const double* gathered, int nparts, long long k, double tol,
@@ -388,7 +433,7 @@ __device__ __forceinline__ void finalize_body(int what, const double* gathered, 
         case kBnorm: decide_bnorm(st, t0); break;
         case kStart: decide_start(st, t0, t1, tol, hist); break;
         case kPq: decide_pq(st, __dadd_rn(t0, t1)); break;  // interior + boundary row sets
-        default: decide_update(st, t0, t1, k, tol, divergence, hist); break;
+        default: decide_update(st, t0, t1, tol, divergence, hist); break;
     }
 }
 

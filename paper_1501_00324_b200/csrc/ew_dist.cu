@@ -933,11 +933,13 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         P->diag.alloc(jacobi ? n : 0);
         P->hist.alloc(cfg.max_iterations + 1);
         const int64_t spmv_blocks = (n + 255) / 256;
-        P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, cg::grid_sum_partials(spmv_blocks)));
-        P->tickets.alloc(std::max<size_t>(1, cg::grid_sum_tickets(spmv_blocks)));
+        P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, cg::dot_partials(spmv_blocks)));
+        P->tickets.alloc(std::max<size_t>(1, cg::dot_tickets(spmv_blocks)));
         EW_CUDA_CHECK(cudaMemsetAsync(P->tickets.get(), 0, P->tickets.bytes(), s));
         P->st.alloc(1);
         EW_CUDA_CHECK(cudaMemsetAsync(P->st.get(), 0, sizeof(cg::State), s));
+        const long long max_it = cfg.max_iterations;
+        EW_CUDA_CHECK(cudaMemcpyAsync(&P->st.get()->max_it, &max_it, sizeof(max_it), cudaMemcpyHostToDevice, s));
         if (ne) {
             EW_CUDA_CHECK(cudaMemsetAsync(P->x_ext.get(), 0, ne * 8, s));
             EW_CUDA_CHECK(cudaMemsetAsync(P->p_ext.get(), 0, ne * 8, s));

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -84,7 +85,10 @@ class DevBuf {
         }
         return *this;
     }
+    // Contents are undefined after alloc (as cudaMalloc's); an allocation of
+    // the same size is kept: cudaMalloc / cudaFree synchronise the device.
     void alloc(size_t n) {
+        if (p_ && n == n_) return;
         release();
         n_ = n;
         if (n) EW_CUDA_CHECK(cudaMalloc(&p_, n * sizeof(T)));
@@ -187,6 +191,41 @@ struct FormatData {
     }
 };
 
+namespace cg {
+struct State;
+}
+
+// Device CG working set, kept between solves: buffers, the pinned polling
+// slots and the CUDA graph of one block of iterations. Reused, a solve does
+// no cudaMalloc / cudaFree / cudaMallocHost (which synchronise the device and
+// can stall it for milliseconds) and no graph capture.
+struct CgWorkspace {
+    std::mutex mu;  // one solve at a time; a concurrent solve gets its own
+    int64_t n = -1;
+    DevBuf<double> r, p, q, x, b, diag, hist, partials;
+    DevBuf<unsigned> tickets;
+    DevBuf<cg::State> st;
+    void* hst = nullptr;  // pinned cg::State[2]
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t per_block = 0;  // launches per graph replay (accounting)
+    // what the graph was captured with
+    double g_tol = 0.0, g_div = 0.0;
+    int64_t g_interval = -1, g_hist = -1;
+    int g_jacobi = -1;
+    CgWorkspace() = default;
+    CgWorkspace(const CgWorkspace&) = delete;
+    CgWorkspace& operator=(const CgWorkspace&) = delete;
+    ~CgWorkspace() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (cap) cudaStreamDestroy(cap);
+        if (ev[0]) cudaEventDestroy(ev[0]);
+        if (ev[1]) cudaEventDestroy(ev[1]);
+        if (hst) cudaFreeHost(hst);
+    }
+};
+
 struct KernelData {
     std::string id;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored_slots = 0;
@@ -196,6 +235,8 @@ struct KernelData {
     std::shared_ptr<LayoutData> layout;  // k1* / k2*
     std::shared_ptr<FormatData> format;  // csr_vector / coo / ell / hyb
     DevBuf<int64_t> entry_dst;           // r / rs: original entry -> reordered entry (refresh)
+    // CG working sets for cg_solve (0) and cg_solve_permuted (1)
+    mutable CgWorkspace cg_ws[2];
 };
 
 std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
@@ -257,9 +298,9 @@ namespace cg {
 struct State;
 }
 struct DotSink {
-    double* partials;   // cg::grid_sum_partials(SpMV CTAs)
+    double* partials;   // cg::dot_partials(SpMV CTAs)
     unsigned capacity;  // partials' length; a larger grid falls back to the dot kernel
-    unsigned* tickets;  // cg::grid_sum_tickets(SpMV CTAs) zeroed counters
+    unsigned* tickets;  // cg::dot_tickets(SpMV CTAs) zeroed counters
     cg::State* st;      // decision / partition total
     int dist;           // 1: store the partition total in st->loc[slot]
     int slot = 0;       // DIST: 0 (also clears loc[1]) or 1 (a second row set)
@@ -305,6 +346,8 @@ struct CgOperator {
     virtual bool apply_dot(const double*, double*, cudaStream_t, const int*, const DotSink&) const { return false; }
     virtual bool host_callback() const { return false; }
     virtual int64_t size() const = 0;
+    // a working set kept between solves with this operator (nullable)
+    virtual CgWorkspace* workspace() const { return nullptr; }
 };
 struct KernelOperator final : CgOperator {
     const KernelData& k;
@@ -317,6 +360,7 @@ struct KernelOperator final : CgOperator {
         return kernel_apply_dot(k, x, y, permuted, s, done, sink);
     }
     int64_t size() const override { return k.nrows == k.ncols ? k.nrows : -1; }
+    CgWorkspace* workspace() const override { return &k.cg_ws[permuted ? 1 : 0]; }
 };
 // Device CG. b, diag, x are device pointers in the operator's numbering.
 CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, int64_t n,

@@ -145,11 +145,11 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
 }
 
 // K1 with the CG's p.q fused in (cg.cpp:72): the operator input x is p, so
-// each row adds x[target] * y[target] to a deterministic two-level grid sum
-// (cg::grid_sum) whose last CTA applies the breakdown test and
-// alpha = rz / pq (or, for a partitioned solve, stores the partition total).
+// each row adds x[target] * y[target] to its CTA's fixed-order partial;
+// cg::dot_final_kernel sums the partials and decides. The CTA only stores
+// its partial: no fence or atomic holds it past its last row.
 template <bool SORTED, bool SCATTER>
-__global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, DotSink sink) {
+__global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -169,14 +169,7 @@ __global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, DotSink sink) 
     }
     pdl_trigger();
     cg::block_sum<1>(v);  // fixed tree per CTA
-    double total;
-    if (!cg::grid_sum(v[0], sink.partials, sink.tickets, &sink.st->ticket, total)) return;
-    if (sink.dist) {
-        sink.st->loc[sink.slot] = total;
-        if (sink.slot == 0) sink.st->loc[1] = 0.0;
-    } else {
-        cg::decide_pq(sink.st, total);
-    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
 }
 
 struct K2Args {
@@ -288,14 +281,17 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
     const unsigned grid = grid_for(l.nrows);
-    if (cg::grid_sum_partials(grid) > sink.capacity) return false;
-    auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink); };
+    if (cg::dot_partials(grid) > sink.capacity) return false;
+    auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink.partials); };
     if (l.sorted) {
         scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
     } else {
         scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
     }
     launched("k1_dot_kernel");
+    launch_pdl(cg::dot_final_kernel, static_cast<unsigned>(cg::dot_final_blocks(grid)), cg::kRedBlock, s,
+               (const double*)sink.partials, grid, sink.partials + grid, sink.tickets, sink.st, sink.dist, sink.slot);
+    launched("cg::dot_final_kernel");
     return true;
 }
 
