@@ -181,7 +181,7 @@ def sum_over_ranks(vals, world):
 # ---------------------------------------------------------------------------
 # CPU: the reference (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------
-def reference_spmv_rate(n, nc, ro, ci, v, kernel="k1", budget_s=15.0, max_calls=50):
+def reference_spmv_rate(n, nc, ro, ci, v, kernel="k1", budget_s=15.0, max_calls=50, warmup=1):
     from oracle.oracle import Csr, Reference
 
     F = Reference()
@@ -191,6 +191,8 @@ def reference_spmv_rate(n, nc, ro, ci, v, kernel="k1", budget_s=15.0, max_calls=
     t0 = time.perf_counter()
     h = F.prepare(kernel, m)
     t_prep = time.perf_counter() - t0
+    for _ in range(warmup):
+        F.run(h, x, y)
     times = []
     t_start = time.perf_counter()
     while len(times) < max_calls and (time.perf_counter() - t_start) < budget_s:
@@ -789,10 +791,10 @@ def run_reference(args, rank, world):
                         "d2h_bytes_per_step": 0}}
     med, calls, t_prep = reference_spmv_rate(n, nc, ro, ci, v, kernel=args.kernel,
                                              budget_s=min(60.0, 3.0 * max(1, args.steps)),
-                                             max_calls=max(args.steps, 1))
+                                             max_calls=max(args.steps, 1), warmup=args.warmup)
     val = 20 * nnz / med / 1e9
     return {"impl": "reference", "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)", "value": round(val, 3),
-            "unit": "GB/s", "n_gpus": world, "steps": calls, "warmup": 0, "ms_per_step": round(med * 1e3, 3),
+            "unit": "GB/s", "n_gpus": world, "steps": calls, "warmup": args.warmup, "ms_per_step": round(med * 1e3, 3),
             "higher_is_better": True, "dtype": "f64",
             "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel},
             "cpu_baseline": {"kind": "reference", "cores": cores, "value": round(val, 3), "unit": "GB/s",
