@@ -407,7 +407,11 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
 
 // Peer transport, first half: push this epoch's values into the peers'
 // ghost tails (on stream s). which: 0 p_ext, 1 x_ext.
-void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+// Owned values come from `src` (per local partition) when given, else from
+// the owned part of ext.
+using PartPtrs = std::vector<const double*>;
+
+void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream_t s, const PartPtrs* src = nullptr) {
     const uint64_t e = ++D.halo_epoch;
     const int32_t G = D.nparts;
     if (!D.ipc) {
@@ -417,11 +421,13 @@ void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream
             launched("ack_kernel");
         }
     }
-    for (auto& P : D.parts) {
+    for (size_t i = 0; i < D.parts.size(); ++i) {
+        auto& P = D.parts[i];
         const int64_t total = static_cast<int64_t>(P->send_idx.size());
         if (!total && (!D.ipc || !P->nsrc)) continue;
         const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(total), 148 * 4));
-        push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), ((*P).*ext).get(), which, e,
+        const double* from = src ? (*src)[i] : ((*P).*ext).get();
+        push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), from, which, e,
                                             P->mboxes.get(), P->part, G, D.ipc ? 1 : 0, P->srcs.get(), P->nsrc,
                                             P->push_ctr.get(), total);
         launched("push_kernel");
@@ -439,18 +445,20 @@ void peer_wait(DistData& D, cudaStream_t s) {
 }
 
 // Exchange the owned values peers need into every partition's ghost tail.
-void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, const PartPtrs* src = nullptr) {
     const int32_t G = D.nparts;
     if (G == 1) return;
     if (D.peer) {
-        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, s);
+        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, s, src);
         peer_wait(D, s);
         return;
     }
-    for (auto& P : D.parts) {
+    for (size_t i = 0; i < D.parts.size(); ++i) {
+        auto& P = D.parts[i];
         const int64_t ns = static_cast<int64_t>(P->send_idx.size());
         if (ns) {
-            pack_kernel<<<grid_for(ns), kBlock, 0, s>>>(P->send_idx.get(), ((*P).*ext).get(), P->send_buf.get(), ns);
+            const double* from = src ? (*src)[i] : ((*P).*ext).get();
+            pack_kernel<<<grid_for(ns), kBlock, 0, s>>>(P->send_idx.get(), from, P->send_buf.get(), ns);
             launched("pack_kernel");
         }
     }
@@ -538,14 +546,14 @@ void reduce_finalize(DistData& D, int what, long long k, const ew_cg_config& cfg
 }
 
 // The exchange on the comm stream, ordered after everything already on s.
-void halo_begin(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s) {
+void halo_begin(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, const PartPtrs* src = nullptr) {
     EW_CUDA_CHECK(cudaEventRecord(D.ev_ready, s));
     EW_CUDA_CHECK(cudaStreamWaitEvent(D.comm_stream, D.ev_ready, 0));
     if (D.peer) {  // the push runs beside the interior rows; peer_wait orders the boundary rows
-        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, D.comm_stream);
+        peer_push(D, ext == &DistPart::x_ext ? 1 : 0, ext, D.comm_stream, src);
         return;
     }
-    halo(D, ext, D.comm_stream);
+    halo(D, ext, D.comm_stream, src);
     EW_CUDA_CHECK(cudaEventRecord(D.ev_halo, D.comm_stream));
 }
 
@@ -562,7 +570,7 @@ void halo_end(DistData& D, cudaStream_t s) {
 // One row set of a split part; with `dot`, its p.q partial goes to loc[slot].
 // False when the fused dot was not available (the caller runs pq_kernel).
 bool run_rows(DistPart& P, const KernelData& k, int64_t nrows, int slot, const double* xe, cudaStream_t s,
-              const int* done, bool dot) {
+              const int* done, bool dot, double* y = nullptr) {
     if (!nrows) {
         if (dot) EW_CUDA_CHECK(cudaMemsetAsync(P.st.get()->loc + slot, 0, (slot == 0 ? 2 : 1) * sizeof(double), s));
         return true;
@@ -571,14 +579,17 @@ bool run_rows(DistPart& P, const KernelData& k, int64_t nrows, int slot, const d
                                 DotSink{P.partials.get(), static_cast<unsigned>(P.partials.size()), P.tickets.get(),
                                         P.st.get(), 1, slot}))
         return true;
-    kernel_apply(k, xe, P.q.get(), false, s, done);
+    kernel_apply(k, xe, y ? y : P.q.get(), false, s, done);
     return !dot;
 }
 
 // q = A x_ext on every local partition after (or, split, overlapped with)
 // the halo exchange of `ext`; dot: p.q into each part's State::loc.
+// xs / ys (split parts, no dot): the caller's owned x and y per partition;
+// the owned x is read in place (interior rows directly, boundary rows with
+// the split-x kernel) and y written in place: only the ghosts go to ext.
 void spmv_exchange(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, bool guard, bool dot,
-                   bool exchange = true) {
+                   bool exchange = true, const PartPtrs* xs = nullptr, const std::vector<double*>* ys = nullptr) {
     std::vector<char> fused(D.parts.size(), 1);
     if (!D.split) {
         if (exchange) halo(D, ext, s);
@@ -587,14 +598,20 @@ void spmv_exchange(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, b
             fused[i] = run_rows(P, *P.op, P.nloc, 0, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr, dot);
         }
     } else {
-        if (exchange) halo_begin(D, ext, s);
+        if (exchange) halo_begin(D, ext, s, xs);
         for (size_t i = 0; i < D.parts.size(); ++i) {
             DistPart& P = *D.parts[i];
-            fused[i] = run_rows(P, *P.op_int, P.n_int, 0, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr, dot);
+            fused[i] = run_rows(P, *P.op_int, P.n_int, 0, xs ? (*xs)[i] : ((P).*ext).get(), s,
+                                guard ? &P.st.get()->done : nullptr, dot, ys ? (*ys)[i] : nullptr);
         }
         if (exchange) halo_end(D, s);
         for (size_t i = 0; i < D.parts.size(); ++i) {
             DistPart& P = *D.parts[i];
+            if (xs) {
+                if (P.n_bnd)
+                    layout_spmv_split(*P.op_bnd->layout, (*xs)[i], ((P).*ext).get() + P.nloc, P.nloc, (*ys)[i], s);
+                continue;
+            }
             fused[i] &= run_rows(P, *P.op_bnd, P.n_bnd, 1, ((P).*ext).get(), s, guard ? &P.st.get()->done : nullptr,
                                  dot);
         }
@@ -905,6 +922,18 @@ void dist_part_info(const DistData& D, int32_t i, int64_t* r0, int64_t* r1, int6
 // y = A x over this process's owned rows (device pointers, concatenated in
 // partition order).
 void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s) {
+    if (D.split) {  // no copies: owned x read in place, y written in place
+        PartPtrs xs;
+        std::vector<double*> ys;
+        int64_t off = 0;
+        for (auto& P : D.parts) {
+            xs.push_back(x + off);
+            ys.push_back(y + off);
+            off += P->nloc;
+        }
+        spmv_exchange(D, &DistPart::x_ext, s, false, false, true, &xs, &ys);
+        return;
+    }
     int64_t off = 0;
     for (auto& P : D.parts) {
         if (P->nloc)

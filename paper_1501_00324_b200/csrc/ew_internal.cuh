@@ -311,6 +311,9 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
 // done (nullable, device): the launch is a no-op once *done != 0 (CG overrun).
 void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
                  const int* done = nullptr);
+// K1 with x split: columns [0, nown) from x, the rest from xg (scatter store).
+void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,
+                       cudaStream_t s);
 void layout_build_slot_map(LayoutData& l, const CsrData& m, cudaStream_t s);
 void layout_refresh_values(LayoutData& l, const CsrData& m, cudaStream_t s);
 int64_t compute_k2_lanes(int64_t nnz_row, int64_t threshold, int64_t warp_size);

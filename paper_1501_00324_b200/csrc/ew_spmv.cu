@@ -44,8 +44,6 @@ __device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
     return v;
 }
 
-__device__ __forceinline__ double ld_x(const double* x, int32_t c) { return __ldg(x + c); }
-
 __device__ __forceinline__ double madd(double acc, double a, double b) {
     return __dadd_rn(acc, __dmul_rn(a, b));  // two roundings, as the reference
 }
@@ -62,6 +60,8 @@ struct K1Args {
     const int* done;
     int64_t nrows, n_active;
     int32_t ws, ws_log2;
+    const double* xg;  // SPLIT_X: columns >= nown read xg[c - nown] (a ghost tail)
+    int32_t nown;
 };
 
 // Serial lane sum over j in [0, mx) at stride `step` from slot s, unrolled by
@@ -69,10 +69,9 @@ struct K1Args {
 // thread before the (order-preserving) accumulation chain consumes them; the
 // last mx % 4 steps go in one predicated block (two round trips, not two per
 // step).
-__device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
-                                           const int32_t* __restrict__ cols,
-                                           const double* __restrict__ x, int64_t s, int64_t step,
-                                           int32_t mx, uint64_t pol) {
+template <typename XLoad>
+__device__ __forceinline__ double lane_sum_x(const double* __restrict__ vals, const int32_t* __restrict__ cols,
+                                             XLoad ld_x, int64_t s, int64_t step, int32_t mx, uint64_t pol) {
     double sum = 0.0;
     int32_t j = 0;
     for (; j + 8 <= mx; j += 8) {
@@ -83,7 +82,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = ld_stream(vals + s + u * step, pol);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = ld_x(x, c[u]);
+        for (int u = 0; u < 8; ++u) xv[u] = ld_x(c[u]);
 #pragma unroll
         for (int u = 0; u < 8; ++u) sum = madd(sum, v[u], xv[u]);
         s += 8 * step;
@@ -96,7 +95,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = ld_stream(vals + s + u * step, pol);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = ld_x(x, c[u]);
+        for (int u = 0; u < 4; ++u) xv[u] = ld_x(c[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) sum = madd(sum, v[u], xv[u]);
         s += 4 * step;
@@ -115,7 +114,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
             if (u < rem) v[u] = ld_stream(vals + s + u * step, pol);
 #pragma unroll
         for (int u = 0; u < 3; ++u)
-            if (u < rem) xv[u] = ld_x(x, c[u]);
+            if (u < rem) xv[u] = ld_x(c[u]);
 #pragma unroll
         for (int u = 0; u < 3; ++u)
             if (u < rem) sum = madd(sum, v[u], xv[u]);
@@ -123,9 +122,24 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals,
     return sum;
 }
 
+__device__ __forceinline__ double lane_sum(const double* __restrict__ vals, const int32_t* __restrict__ cols,
+                                           const double* __restrict__ x, int64_t s, int64_t step, int32_t mx,
+                                           uint64_t pol) {
+    return lane_sum_x(vals, cols, [x](int32_t c) { return __ldg(x + c); }, s, step, mx, pol);
+}
+
+// x split in two arrays: owned columns [0, nown) in x, the ghost tail in xg
+// (a partition's local columns; the caller's x needs no copy).
+__device__ __forceinline__ double lane_sum_split(const double* __restrict__ vals, const int32_t* __restrict__ cols,
+                                                 const double* __restrict__ x, const double* __restrict__ xg,
+                                                 int32_t nown, int64_t s, int64_t step, int32_t mx, uint64_t pol) {
+    return lane_sum_x(vals, cols, [x, xg, nown](int32_t c) { return c < nown ? __ldg(x + c) : __ldg(xg + (c - nown)); },
+                      s, step, mx, pol);
+}
+
 // K1 / K1r / K1rs (warp_spmv.cpp:9-60): one thread per sorted row position.
 // SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
-template <bool SORTED, bool SCATTER, bool ROW_MAJOR>
+template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false>
 __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
     pdl_wait();
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -138,7 +152,8 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
         const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
         const int32_t mx = a.maxrows[w];
         const int64_t s = a.woff[w] + (ROW_MAJOR ? int64_t(lane) * mx : lane);
-        sum = lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
+        sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, ROW_MAJOR ? 1 : a.ws, mx, pol)
+                      : lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
     }
     a.y[SCATTER ? a.fwd[p] : p] = sum;
     pdl_trigger();
@@ -279,7 +294,7 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
                      const int* done, const DotSink& sink) {
     if (l.kind != EW_LAYOUT_K1 || l.row_major || l.nrows == 0) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
-             l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
+             l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
     auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink.partials); };
@@ -300,7 +315,7 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     if (l.nrows == 0) return;
     if (l.kind == EW_LAYOUT_K1) {
         K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
-                 l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2};
+                 l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
         const bool rm = l.row_major != 0;
         if (l.sorted) {
             scatter ? launch_k1<true, true>(a, rm, s) : launch_k1<true, false>(a, rm, s);
@@ -321,6 +336,19 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     } else {
         scatter ? launch_k2<false, true>(a, s) : launch_k2<false, false>(a, s);
     }
+}
+
+void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,
+                       cudaStream_t s) {
+    require(l.kind == EW_LAYOUT_K1 && !l.row_major, "split-x SpMV: K1 column-major layouts only");
+    if (l.nrows == 0) return;
+    K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
+             l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, xg, static_cast<int32_t>(nown)};
+    if (l.sorted)
+        launch_pdl(k1_kernel<true, true, false, true>, grid_for(a.nrows), kBlock, s, a);
+    else
+        launch_pdl(k1_kernel<false, true, false, true>, grid_for(a.nrows), kBlock, s, a);
+    launched("k1_kernel");
 }
 
 }  // namespace ew
