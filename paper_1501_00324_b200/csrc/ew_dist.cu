@@ -174,7 +174,12 @@ struct DistData {
     bool split = false;                    // every part has op_int / op_bnd
     cudaStream_t comm_stream = nullptr;    // halo exchange, concurrent with the interior rows
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    void* hst = nullptr;                   // pinned cg::State[2] for CG polling
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     ~DistData() {
+        if (hst) cudaFreeHost(hst);
+        for (auto e : poll_ev)
+            if (e) cudaEventDestroy(e);
         for (void* p : ipc_mapped) cudaIpcCloseMemHandle(p);
         if (ev_ready) cudaEventDestroy(ev_ready);
         if (ev_halo) cudaEventDestroy(ev_halo);
@@ -1029,18 +1034,16 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
     reduce_finalize(D, cg::kStart, 0, cfg, s);
 
     DistPart& P0 = *D.parts[0];
-    cg::State* hst = nullptr;
-    EW_CUDA_CHECK(cudaMallocHost(&hst, 2 * sizeof(cg::State)));
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    auto cleanup = [&] {
-        if (ev[0]) cudaEventDestroy(ev[0]);
-        if (ev[1]) cudaEventDestroy(ev[1]);
-        cudaFreeHost(hst);
-    };
+    // pinned polling slots and events kept on the operator (cudaMallocHost
+    // per solve can stall the device)
+    if (!D.hst) EW_CUDA_CHECK(cudaMallocHost(&D.hst, 2 * sizeof(cg::State)));
+    for (auto& e : D.poll_ev)
+        if (!e) EW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cg::State* hst = static_cast<cg::State*>(D.hst);
+    cudaEvent_t* ev = D.poll_ev;
+    auto cleanup = [] {};
     cg::State h{};
     try {
-        EW_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-        EW_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
         int64_t it = 1;
         int batch = 8, j = 0;
         while (it <= cfg.max_iterations) {
