@@ -28,9 +28,14 @@ struct PreparedKernel {
 // csr_ref, csr_vector, coo, ell, hyb, k1, k1r, k1rs, k2, k2r, k2rs
 const std::vector<std::string>& kernel_ids();
 
+enum class RowOrder : idx { reference = 0, locality = 1 };
+
 struct KernelOptions {
     idx k2_threshold = 0;  // <= 0: max row length
     idx hyb_k_ell = -1;    // < 0: 2/3-coverage heuristic
+    // not in the reference: r / rs kernels may group rows by a Cuthill-McKee
+    // order under the longest-first sort (same row sums; perm = that order)
+    RowOrder row_order = RowOrder::reference;
 };
 
 PreparedKernel prepare_kernel(const std::string& id, const SparseCsr& m, const WarpModelConfig& cfg,

@@ -17,7 +17,7 @@ PreparedKernel prepare_kernel(const std::string& id, const SparseCsr& m, const W
     cfg.validate();
     auto h = device::upload(m);
     const ew_warp_config c = device::to_c(cfg);
-    const ew_kernel_options o{opts.k2_threshold, opts.hyb_k_ell};
+    const ew_kernel_options o{opts.k2_threshold, opts.hyb_k_ell, static_cast<int64_t>(opts.row_order)};
     ew_kernel k = nullptr;
     device::check(ew_kernel_prepare(id.c_str(), h.get(), &c, &o, &k));
     device::KernelHandle kh(k, [](ew_kernel p) { ew_kernel_destroy(p); });

@@ -204,3 +204,25 @@ def test_resident_prepared_kernel(ew_mod, ew, R, F):
     h = np.asarray(res["residual_history"])
     assert np.all(np.abs(h - ref.residual_history) <= 1e-10 * (1 + ref.residual_history))
     assert math.isclose(res["solution"][0], 1.0, rel_tol=1e-6)
+
+
+@pytest.mark.gpu
+def test_prepare_kernel_locality_row_order(ew_mod, ew, R):
+    """KernelOptions::row_order = locality through the C++ API / _ellwarp:
+    same row sums as the reference kernel, CG within the comparator."""
+    from oracle.oracle import Csr
+
+    m = ew_mod.laplacian3d(9, 8, 7)
+    mo = Csr.make(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+    x = np.linspace(0.1, 1.0, m.ncols)
+    for kid in ("k1r", "k1rs"):
+        k = ew_mod.prepare_kernel(kid, m, row_order="locality")
+        assert np.array_equal(k.apply(x), ew_mod.prepare_kernel(kid, m).apply(x))
+        b = ew_mod.spmv_reference(m, [1.0] * m.ncols)
+        res = k.cg_solve(np.asarray(b), ew_mod.extract_diagonal(m), permuted=True)
+        ref = R.cg_csr(mo, b)
+        assert res["iterations"] == ref.iterations
+        h = np.asarray(res["residual_history"])
+        assert np.all(np.abs(h - ref.residual_history) <= 1e-10 * (1 + ref.residual_history))
+    with pytest.raises(ValueError):
+        ew_mod.prepare_kernel("k1", m, row_order="locality")
