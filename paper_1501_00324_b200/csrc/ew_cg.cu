@@ -1,17 +1,21 @@
 // Single-GPU Jacobi PCG driver (cg.cpp:25-104): the prepared kernel (or a
 // host closure) is the operator, everything else stays on the device.
 //
-// Per iteration four stream-ordered launches, no host round trip:
-//   1. q = A p                        (operator)
-//   2. p.q                            (+ breakdown test, alpha = rz / pq)
-//   3. x += alpha p ; r -= alpha q    (+ r.r, r.z with z = r / diag, history,
-//                                      convergence / divergence, beta)
+// Per iteration, stream-ordered, no host round trip:
+//   1. q = A p, with one p.q partial per SpMV CTA   (operator)
+//   2. p.q summed in a fixed order                  (+ breakdown test, alpha)
+//   3. x += alpha p ; r -= alpha q                  (+ r.r, r.z with z = r / diag,
+//                                                    history, convergence /
+//                                                    divergence, beta)
 //      refresh iterations (k % recompute_interval == 0) replace the r update
 //      by r = b - A x after one more operator launch, as cg.cpp:82-86
 //   4. p = z + beta p
 // Element-wise arithmetic follows the reference exactly; dot products are
-// fixed-order trees (ew_cg.cuh). Kernels read a device `done` flag first, so
-// the host enqueues iterations in batches and polls once per batch.
+// fixed-order trees (ew_cg.cuh). The iteration counter and a `done` flag live
+// on the device, so one refresh interval of iterations is captured once into
+// a CUDA graph and replayed; the host polls the state once per replay. The
+// working set (vectors, partials, polling slots, graph) stays with the
+// prepared kernel between solves.
 #include "ew_cg.cuh"
 
 namespace ew {
@@ -111,13 +115,13 @@ CgOutputs cg_run(const CgOperator& op, CgWorkspace& w, const double* b_in, const
         }
         const bool refresh = interval > 0 && k % interval == 0;
         launch_pdl(cg::update_kernel<false>, g_up, cg::kRedBlock, t, refresh ? 1 : 0, x, r, (const double*)p,
-                   (const double*)q, (const double*)b, diag, n, jacobi, (long long)k, cfg.rel_tolerance,
+                   (const double*)q, (const double*)b, diag, n, jacobi, cfg.rel_tolerance,
                    cfg.divergence_limit, partials, st, hist);
         launched("cg::update_kernel");
         if (refresh) {
             if (!(host_op && host_done())) op.apply(x, q, t, done);
             launch_pdl(cg::update_kernel<false>, g_up, cg::kRedBlock, t, 2, x, r, (const double*)p, (const double*)q,
-                       (const double*)b, diag, n, jacobi, (long long)k, cfg.rel_tolerance, cfg.divergence_limit,
+                       (const double*)b, diag, n, jacobi, cfg.rel_tolerance, cfg.divergence_limit,
                        partials, st, hist);
             launched("cg::update_kernel");
         }

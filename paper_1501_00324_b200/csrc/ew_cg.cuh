@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __r
                                                            const double* __restrict__ p, const double* __restrict__ q,
                                                            const double* __restrict__ b,
                                                            const double* __restrict__ diag, int64_t n, int jacobi,
-                                                           long long k, double tol, double divergence,
+                                                           double tol, double divergence,
                                                            double* partials, State* st, double* hist) {
     pdl_wait();
     if (st->done) return;
@@ -421,7 +421,7 @@ inline size_t dot_partials(int64_t blocks) {
 inline size_t dot_tickets(int64_t blocks) { return grid_sum_tickets(static_cast<int64_t>(dot_final_blocks(blocks))); }
 
 // DIST: sum the all-gathered partition totals in rank order, then decide.
-__device__ __forceinline__ void finalize_body(int what, const double* gathered, int nparts, long long k, double tol,
+__device__ __forceinline__ void finalize_body(int what, const double* gathered, int nparts, double tol,
                                               double divergence, State* st, double* hist) {
     if (what != kBnorm && what != kStart && st->done) return;
     double t0 = 0.0, t1 = 0.0;
@@ -437,9 +437,9 @@ __device__ __forceinline__ void finalize_body(int what, const double* gathered, 
     }
 }
 
-static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, long long k,
-                                       double tol, double divergence, State* st, double* hist) {
-    finalize_body(what, gathered, nparts, k, tol, divergence, st, hist);
+static __global__ void finalize_kernel(int what, const double* __restrict__ gathered, int nparts, double tol,
+                                       double divergence, State* st, double* hist) {
+    finalize_body(what, gathered, nparts, tol, divergence, st, hist);
 }
 
 inline unsigned red_grid(int64_t n) {

@@ -283,7 +283,7 @@ __global__ void collect_kernel(const uint64_t* mine, int G, uint64_t epoch, doub
 // collect_kernel and cg::finalize_kernel in one launch: thread g waits for
 // partition g's totals, thread 0 sums them in rank order and decides.
 __global__ void collect_finalize_kernel(const uint64_t* mine, int G, uint64_t epoch, double* gathered, int what,
-                                        long long k, double tol, double divergence, cg::State* st, double* hist) {
+                                        double tol, double divergence, cg::State* st, double* hist) {
     const int g = threadIdx.x;
     if (g < G) {
         spin_until(mine + Mbox::red(G, g), epoch);
@@ -292,7 +292,7 @@ __global__ void collect_finalize_kernel(const uint64_t* mine, int G, uint64_t ep
         gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) cg::finalize_body(what, gathered, G, k, tol, divergence, st, hist);
+    if (threadIdx.x == 0) cg::finalize_body(what, gathered, G, tol, divergence, st, hist);
 }
 
 // Ghost columns of a row block [r0, r1) given with global column ids:
@@ -521,9 +521,9 @@ void allgather(DistData& D, cudaStream_t s) {
                                           cudaMemcpyDeviceToDevice, s));
 }
 
-void finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaStream_t s) {
+void finalize(DistData& D, int what, const ew_cg_config& cfg, cudaStream_t s) {
     for (auto& P : D.parts) {
-        cg::finalize_kernel<<<1, 1, 0, s>>>(what, P->gathered.get(), D.nparts, k, cfg.rel_tolerance,
+        cg::finalize_kernel<<<1, 1, 0, s>>>(what, P->gathered.get(), D.nparts, cfg.rel_tolerance,
                                             cfg.divergence_limit, P->st.get(), P->hist.get());
         launched("cg::finalize_kernel");
     }
@@ -531,10 +531,10 @@ void finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaS
 
 // A CG reduction: every partition's State::loc totals summed in rank order on
 // every partition, then the reference's decision.
-void reduce_finalize(DistData& D, int what, long long k, const ew_cg_config& cfg, cudaStream_t s) {
+void reduce_finalize(DistData& D, int what, const ew_cg_config& cfg, cudaStream_t s) {
     if (!D.peer) {
         allgather(D, s);
-        finalize(D, what, k, cfg, s);
+        finalize(D, what, cfg, s);
         return;
     }
     const uint64_t e = ++D.red_epoch;
@@ -543,7 +543,7 @@ void reduce_finalize(DistData& D, int what, long long k, const ew_cg_config& cfg
         launched("publish_kernel");
     }
     for (auto& P : D.parts) {
-        collect_finalize_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, e, P->gathered.get(), what, k,
+        collect_finalize_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, e, P->gathered.get(), what,
                                                  cfg.rel_tolerance, cfg.divergence_limit, P->st.get(),
                                                  P->hist.get());
         launched("collect_finalize_kernel");
@@ -990,7 +990,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                                                                               jacobi, P->partials.get(), P->st.get());
         launched("cg::init_kernel<dist>");
     }
-    reduce_finalize(D, cg::kBnorm, 0, cfg, s);
+    reduce_finalize(D, cg::kBnorm, cfg, s);
     std::vector<cg::State> hs(D.parts.size());
     for (size_t i = 0; i < D.parts.size(); ++i)
         EW_CUDA_CHECK(cudaMemcpyAsync(&hs[i], D.parts[i]->st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
@@ -1031,7 +1031,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
             P->partials.get(), P->st.get(), P->hist.get());
         launched("cg::start_kernel<dist>");
     }
-    reduce_finalize(D, cg::kStart, 0, cfg, s);
+    reduce_finalize(D, cg::kStart, cfg, s);
 
     DistPart& P0 = *D.parts[0];
     // pinned polling slots and events kept on the operator (cudaMallocHost
@@ -1050,7 +1050,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
             const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
             for (; it <= last; ++it) {
                 spmv_exchange(D, &DistPart::p_ext, s, true, true);
-                reduce_finalize(D, cg::kPq, it, cfg, s);
+                reduce_finalize(D, cg::kPq, cfg, s);
                 const bool refresh = cfg.recompute_interval > 0 && it % cfg.recompute_interval == 0;
                 for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
                     if (mode < 0) break;
@@ -1060,12 +1060,12 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
                                                                     P->nloc),
                                                   cg::kRedBlock, 0, s>>>(
                             mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
-                            P->nloc, jacobi, it, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(),
+                            P->nloc, jacobi, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(),
                             P->st.get(), P->hist.get());
                         launched("cg::update_kernel<dist>");
                     }
                 }
-                reduce_finalize(D, cg::kUpdate, it, cfg, s);
+                reduce_finalize(D, cg::kUpdate, cfg, s);
                 for (auto& P : D.parts) {
                     cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, s>>>(P->p_ext.get(), P->r.get(), P->diag.get(),
                                                                           P->nloc, jacobi, P->st.get());
