@@ -79,6 +79,44 @@ def cases(F):
             yield f"random{i}", m
 
 
+def _block_diagonal(nblocks, size, seed):
+    """nblocks disconnected path graphs (SPD tridiagonal blocks), shuffled."""
+    n = nblocks * size
+    rows, cols = [], []
+    for b in range(nblocks):
+        for i in range(size):
+            r = b * size + i
+            for c in (r - 1, r, r + 1):
+                if b * size <= c < (b + 1) * size:
+                    rows.append(r)
+                    cols.append(c)
+    perm = np.random.default_rng(seed).permutation(n)
+    rows, cols = perm[np.array(rows)], perm[np.array(cols)]
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    ro = np.zeros(n + 1, np.int64)
+    np.add.at(ro, rows + 1, 1)
+    ro = np.cumsum(ro)
+    vals = np.where(rows == cols, 4.0, -1.0)
+    return Csr.make(n, n, ro, cols.astype(np.int64), vals)
+
+
+def test_edge_cases(ew, R, F):
+    """Empty rows, one row, and more components than the BFS restarts
+    (the rest is appended in row order)."""
+    cases_ = [("components", _block_diagonal(100, 3, 1)), ("one", Csr.make(1, 1, [0, 1], [0], [2.0]))]
+    m = F.random_csr(60, 60, 0.05, 8, empty=0.3)
+    cases_.append(("empty_rows", m))
+    for name, m in cases_:
+        a = dev(ew, m)
+        x = F.random_vector(m.ncols, 3)
+        for kid in ("k1r", "k1rs"):
+            k = ew.Kernel(kid, a, row_order="locality")
+            fwd, _ = k.perm()
+            assert np.array_equal(fwd, locality_order(m.row_offsets, m.col_indices, m.nrows)), (name, kid)
+            assert np.array_equal(k.apply(x), oracle_apply(R, kid, m, x)), (name, kid)
+
+
 def test_order_matches_restatement(ew, F):
     for name, m in cases(F):
         a = dev(ew, m)
