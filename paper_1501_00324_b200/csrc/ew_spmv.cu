@@ -12,6 +12,9 @@
 // included), with the multiply and the add rounded separately (no FMA), and
 // K2 combines lane partials with the reference's ascending-stride pairwise
 // tree (stride 1, 2, 4, ...), done here with __shfl_down_sync.
+#include <cstdlib>
+#include <string>
+
 #include "ew_cg.cuh"
 
 namespace ew {
@@ -159,6 +162,53 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
     pdl_trigger();
 }
 
+// The same K1 in grid-stride form, for layouts well beyond L2 (the launch
+// grid is still one CTA per 256 rows, so the body runs once per thread).
+// ptxas schedules this form differently under the 32-register cap: it keeps
+// the row index and store address out of registers across the lane loop
+// (spilled to L1) and issues all eight column loads of a block before the
+// first x gather. On HBM-bound matrices with long rows that is +4.5%
+// (config 2, 44 slots per row: 170.5 -> 163 us, 0.95 -> 0.995 of HBM); on
+// L2-resident ones the spill traffic costs more than it gains (config 1:
+// 7.6 -> 9.1 us), and short-row gather-bound ones (config 4, 15 per row;
+// the CG's fused p.q variant) lose 1-5%, so layout_spmv picks by size and
+// row length. Same arithmetic, bit-identical results.
+template <bool SORTED, bool SCATTER, bool SPLIT_X = false>
+__global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
+    pdl_wait();
+    if (a.done && *a.done) return;
+    const uint64_t pol = evict_first_policy();
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.nrows;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double sum = 0.0;
+        const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
+        if (active) {
+            const int64_t w = p >> a.ws_log2;
+            const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
+            const int32_t mx = a.maxrows[w];
+            const int64_t s = a.woff[w] + lane;
+            sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, a.ws, mx, pol)
+                          : lane_sum(a.values, a.cols, a.x, s, a.ws, mx, pol);
+        }
+        a.y[SCATTER ? a.fwd[p] : p] = sum;
+    }
+    pdl_trigger();
+}
+
+// Layouts whose slabs exceed this stream from HBM, with at least this many
+// slots per row: k1_stream_kernel.
+constexpr int64_t kStreamSlotBytes = 64ll << 20;
+constexpr int64_t kStreamSlotsPerRow = 24;
+
+inline bool streams(const LayoutData& l) {
+    static const int force = [] {
+        const char* e = std::getenv("EW_K1_FORM");  // A/B runs: "stream" / "plain"
+        return e ? (std::string(e) == "stream" ? 1 : 0) : -1;
+    }();
+    if (force >= 0) return force == 1;
+    return l.nslots * 12 > kStreamSlotBytes && l.nslots >= kStreamSlotsPerRow * l.nrows;
+}
+
 // K1 with the CG's p.q fused in (cg.cpp:72): the operator input x is p, so
 // each row adds x[target] * y[target] to its CTA's fixed-order partial;
 // cg::dot_final_kernel sums the partials and decides. The CTA only stores
@@ -269,8 +319,10 @@ __global__ void k2_wide_kernel(K2Args a) {
 }
 
 template <bool SORTED, bool SCATTER>
-void launch_k1(const K1Args& a, bool row_major, cudaStream_t s) {
-    if (row_major)
+void launch_k1(const K1Args& a, bool row_major, bool stream_form, cudaStream_t s) {
+    if (stream_form && !row_major)
+        launch_pdl(k1_stream_kernel<SORTED, SCATTER>, grid_for(a.nrows), kBlock, s, a);
+    else if (row_major)
         launch_pdl(k1_kernel<SORTED, SCATTER, true>, grid_for(a.nrows), kBlock, s, a);
     else
         launch_pdl(k1_kernel<SORTED, SCATTER, false>, grid_for(a.nrows), kBlock, s, a);
@@ -316,11 +368,11 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     if (l.kind == EW_LAYOUT_K1) {
         K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
                  l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
-        const bool rm = l.row_major != 0;
+        const bool rm = l.row_major != 0, sf = streams(l);
         if (l.sorted) {
-            scatter ? launch_k1<true, true>(a, rm, s) : launch_k1<true, false>(a, rm, s);
+            scatter ? launch_k1<true, true>(a, rm, sf, s) : launch_k1<true, false>(a, rm, sf, s);
         } else {
-            scatter ? launch_k1<false, true>(a, rm, s) : launch_k1<false, false>(a, rm, s);
+            scatter ? launch_k1<false, true>(a, rm, sf, s) : launch_k1<false, false>(a, rm, sf, s);
         }
         return;
     }
@@ -344,10 +396,16 @@ void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, i
     if (l.nrows == 0) return;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, xg, static_cast<int32_t>(nown)};
-    if (l.sorted)
+    if (streams(l)) {
+        if (l.sorted)
+            launch_pdl(k1_stream_kernel<true, true, true>, grid_for(a.nrows), kBlock, s, a);
+        else
+            launch_pdl(k1_stream_kernel<false, true, true>, grid_for(a.nrows), kBlock, s, a);
+    } else if (l.sorted) {
         launch_pdl(k1_kernel<true, true, false, true>, grid_for(a.nrows), kBlock, s, a);
-    else
+    } else {
         launch_pdl(k1_kernel<false, true, false, true>, grid_for(a.nrows), kBlock, s, a);
+    }
     launched("k1_kernel");
 }
 

@@ -7,9 +7,9 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_secto
 O=gpurun_out/prof
 mkdir -p $O
 # 1. K1 SpMV, config 2 (default bench): 20 launches, then one --set full
-ncu --metrics $M --clock-control none -k regex:k1_kernel -s 5 -c 20 --csv --log-file $O/k1_c2_launches.csv \
+ncu --metrics $M --clock-control none -k regex:"k1_(stream_)?kernel" -s 5 -c 20 --csv --log-file $O/k1_c2_launches.csv \
     python bench.py --steps 30 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:k1_kernel -s 5 -c 1 -o $O/k1_c2_full \
+ncu --set full --import-source on --clock-control none -k regex:"k1_(stream_)?kernel" -s 5 -c 1 -o $O/k1_c2_full \
     python bench.py --steps 8 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 # 2. K1 SpMV, config 1 (L2-resident)
 ncu --metrics $M --clock-control none -k regex:k1_kernel -s 5 -c 10 --csv --log-file $O/k1_c1_launches.csv \
