@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict_
 // mode 1: x += alpha p only (refresh iteration, first half)
 // mode 2: r = b - A x (A x in q), then r.r, r.z       (cg.cpp:82-86)
 template <bool DIST>
-__global__ void __launch_bounds__(kRedBlock) update_kernel(int mode, double* __restrict__ x, double* __restrict__ r,
+__global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* __restrict__ x, double* __restrict__ r,
                                                            const double* __restrict__ p, const double* __restrict__ q,
                                                            const double* __restrict__ b,
                                                            const double* __restrict__ diag, int64_t n, int jacobi,

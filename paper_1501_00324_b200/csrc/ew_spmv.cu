@@ -170,9 +170,10 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
 // first x gather. On HBM-bound matrices with long rows that is +4.5%
 // (config 2, 44 slots per row: 170.5 -> 163 us, 0.95 -> 0.995 of HBM); on
 // L2-resident ones the spill traffic costs more than it gains (config 1:
-// 7.6 -> 9.1 us), and short-row gather-bound ones (config 4, 15 per row;
-// the CG's fused p.q variant) lose 1-5%, so layout_spmv picks by size and
-// row length. Same arithmetic, bit-identical results.
+// 7.6 -> 9.1 us), and short-row gather-bound ones (config 4, 15 per row)
+// lose 1-5%, so layout_spmv picks by size and row length (the CG's fused
+// p.q kernel likewise: config-2-sized slab CG +4.8%). Same arithmetic,
+// bit-identical results.
 template <bool SORTED, bool SCATTER, bool SPLIT_X = false>
 __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
     pdl_wait();
@@ -231,6 +232,31 @@ __global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, double* __rest
         const int64_t t = SCATTER ? a.fwd[p] : p;
         a.y[t] = sum;
         v[0] = __dmul_rn(a.x[t], sum);
+    }
+    pdl_trigger();
+    cg::block_sum<1>(v);  // fixed tree per CTA
+    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+}
+
+// k1_dot_kernel in the grid-stride form of k1_stream_kernel (large long-row layouts).
+template <bool SORTED, bool SCATTER>
+__global__ void __launch_bounds__(256, 8) k1_dot_stream_kernel(K1Args a, double* __restrict__ partials) {
+    pdl_wait();
+    if (a.done && *a.done) return;  // uniform across the grid
+    const uint64_t pol = evict_first_policy();
+    double v[1] = {0.0};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < a.nrows;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double sum = 0.0;
+        const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
+        if (active) {
+            const int64_t w = p >> a.ws_log2;
+            const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
+            sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+        }
+        const int64_t t = SCATTER ? a.fwd[p] : p;
+        a.y[t] = sum;
+        v[0] = __dadd_rn(v[0], __dmul_rn(a.x[t], sum));
     }
     pdl_trigger();
     cg::block_sum<1>(v);  // fixed tree per CTA
@@ -350,7 +376,12 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
     auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink.partials); };
-    if (l.sorted) {
+    if (streams(l)) {
+        if (l.sorted)
+            scatter ? go(k1_dot_stream_kernel<true, true>) : go(k1_dot_stream_kernel<true, false>);
+        else
+            scatter ? go(k1_dot_stream_kernel<false, true>) : go(k1_dot_stream_kernel<false, false>);
+    } else if (l.sorted) {
         scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
     } else {
         scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
