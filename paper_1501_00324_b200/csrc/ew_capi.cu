@@ -720,6 +720,7 @@ ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, v
         const int64_t n = ew::dist_owned_rows(*d->d);
         with_io(x, n, y, n, mem, ew::as_stream(stream),
                 [&](const double* xd, double* yd) { ew::dist_spmv(*d->d, xd, yd, ew::as_stream(stream)); });
+        if (mem == EW_MEM_HOST) ew::dist_check_peers(*d->d, ew::as_stream(stream));  // synchronised anyway
     });
 }
 

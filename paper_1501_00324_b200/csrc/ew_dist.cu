@@ -124,7 +124,8 @@ struct PushDesc {
 
 // Mailbox words of a partition in a G-way peer transport.
 struct Mbox {
-    __host__ __device__ static size_t words(int32_t G) { return 7 * static_cast<size_t>(G); }
+    __host__ __device__ static size_t words(int32_t G) { return 7 * static_cast<size_t>(G) + 1; }
+    __host__ __device__ static size_t err(int32_t G) { return 7 * static_cast<size_t>(G); }  // a wait timed out
     __host__ __device__ static size_t halo(int32_t g) { return g; }                       // halo epoch raised by g
     __host__ __device__ static size_t ack(int32_t G, int32_t g) { return G + g; }         // g consumed this rank's epoch
     __host__ __device__ static size_t red(int32_t G, int32_t g) { return 2 * G + g; }     // reduction epoch raised by g
@@ -207,8 +208,21 @@ __device__ __forceinline__ double ld_relaxed_sys(const double* p) {
     return v;
 }
 
-__device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t e) {
-    while (ld_acquire_sys(p) < e) __nanosleep(64);
+// Bounded wait: a peer that never answers (a dead rank) must not hang the
+// GPU. After ~30 s of cycles the partition's error word is set, every later
+// wait returns at once, and the host reports the failure after the solve.
+constexpr long long kSpinLimitCycles = 60'000'000'000ll;
+
+__device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t e, uint64_t* err) {
+    if (ld_acquire_sys(err)) return;
+    const long long t0 = clock64();
+    while (ld_acquire_sys(p) < e) {
+        if (clock64() - t0 > kSpinLimitCycles) {
+            atomicExch(reinterpret_cast<unsigned long long*>(err), 1ull);
+            return;
+        }
+        __nanosleep(64);
+    }
 }
 
 // Pack and transfer in one kernel: the owned values each destination needs
@@ -225,7 +239,8 @@ __global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int
     uint64_t* mine = mboxes[me];
     if (write_acks && blockIdx.x == 0)
         for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch - 1);
-    for (int i = threadIdx.x; i < ndesc; i += blockDim.x) spin_until(mine + Mbox::ack(G, d[i].peer), epoch - 1);
+    for (int i = threadIdx.x; i < ndesc; i += blockDim.x)
+        spin_until(mine + Mbox::ack(G, d[i].peer), epoch - 1, mine + Mbox::err(G));
     __syncthreads();
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
         int i = 0;
@@ -252,8 +267,8 @@ __global__ void ack_kernel(uint64_t* const* mboxes, int me, int G, const int32_t
 }
 
 // The ghost tail is complete once every source raised this epoch.
-__global__ void halo_wait_kernel(const uint64_t* mine, const int32_t* __restrict__ srcs, int nsrc, uint64_t epoch) {
-    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) spin_until(mine + Mbox::halo(srcs[i]), epoch);
+__global__ void halo_wait_kernel(uint64_t* mine, int G, const int32_t* __restrict__ srcs, int nsrc, uint64_t epoch) {
+    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) spin_until(mine + Mbox::halo(srcs[i]), epoch, mine + Mbox::err(G));
 }
 
 // Reduction, step 1: this partition's totals (State::loc) into slot `me` of
@@ -271,10 +286,10 @@ __global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int
 
 // Reduction, step 2: wait for every partition's totals, copy them to
 // `gathered` in rank order (then cg::finalize_kernel sums them).
-__global__ void collect_kernel(const uint64_t* mine, int G, uint64_t epoch, double* gathered) {
+__global__ void collect_kernel(uint64_t* mine, int G, uint64_t epoch, double* gathered) {
     const int g = threadIdx.x;
     if (g >= G) return;
-    spin_until(mine + Mbox::red(G, g), epoch);
+    spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
     const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
     gathered[2 * g] = ld_relaxed_sys(v);
     gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
@@ -282,11 +297,11 @@ __global__ void collect_kernel(const uint64_t* mine, int G, uint64_t epoch, doub
 
 // collect_kernel and cg::finalize_kernel in one launch: thread g waits for
 // partition g's totals, thread 0 sums them in rank order and decides.
-__global__ void collect_finalize_kernel(const uint64_t* mine, int G, uint64_t epoch, double* gathered, int what,
+__global__ void collect_finalize_kernel(uint64_t* mine, int G, uint64_t epoch, double* gathered, int what,
                                         double tol, double divergence, cg::State* st, double* hist) {
     const int g = threadIdx.x;
     if (g < G) {
-        spin_until(mine + Mbox::red(G, g), epoch);
+        spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
         const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
         gathered[2 * g] = ld_relaxed_sys(v);
         gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
@@ -444,7 +459,7 @@ void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream
 void peer_wait(DistData& D, cudaStream_t s) {
     for (auto& P : D.parts) {
         if (!P->nsrc) continue;
-        halo_wait_kernel<<<1, 32, 0, s>>>(P->mbox.get(), P->srcs.get(), P->nsrc, D.halo_epoch);
+        halo_wait_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, P->srcs.get(), P->nsrc, D.halo_epoch);
         launched("halo_wait_kernel");
     }
 }
@@ -909,6 +924,16 @@ std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* 
     return D;
 }
 
+void dist_check_peers(const DistData& D, cudaStream_t s) {
+    if (!D.peer) return;
+    for (auto& P : D.parts) {
+        uint64_t err = 0;
+        EW_CUDA_CHECK(cudaMemcpyAsync(&err, P->mbox.get() + Mbox::err(D.nparts), sizeof(err), cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (err) throw Error(EW_CUDA, "peer transport: a peer did not answer within ~30 s (rank failure?)");
+    }
+}
+
 int64_t dist_owned_rows(const DistData& D) {
     int64_t n = 0;
     for (auto& P : D.parts) n += P->nloc;
@@ -1096,6 +1121,7 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         off += P->nloc;
     }
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    dist_check_peers(D, s);
     return cg_outputs(h.status, h.iterations, cfg, P0.hist.get());
 }
 
