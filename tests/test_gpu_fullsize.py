@@ -102,3 +102,16 @@ def test_config4_cg_properties(ew, R, c4):
     its = runs["reference"].iterations
     assert abs(its - runs["locality"].iterations) <= max(1, its // 100)
     assert np.allclose(runs["reference"].solution, runs["locality"].solution, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_config2_partitioned_spmv_bitwise(ew, c2, transport):
+    """Config 2 in 4 row blocks on one GPU (interior rows overlapping the
+    halo, boundary rows after it): bitwise the single-GPU K1."""
+    a = dev(ew, c2)
+    x = np.random.default_rng(4).uniform(0.1, 1.0, c2.ncols)
+    single = ew.Kernel("k1", a).apply(x)
+    d = ew.Dist.local(c2, 4, transport=transport)
+    y = d.spmv(x)
+    both_zero = (y == 0) & (single == 0)
+    assert np.all(both_zero | (bits(y) == bits(single)))
