@@ -451,6 +451,8 @@ static ew_status apply_impl(ew_kernel k, const double* x, int64_t nx, double* y,
             throw ew::Error(EW_INVALID_ARGUMENT, "kernel '" + d.id + "' has no apply_permuted");
         ew::require(nx == d.ncols, "spmv dimension mismatch");
         ew::require(ny == d.nrows, "spmv output length mismatch");
+        // large plain K1 with host buffers: copies overlapped with compute
+        if (mem == EW_MEM_HOST && !permuted && ew::kernel_apply_host(d, x, y, ew::as_stream(stream))) return;
         with_io(x, nx, y, ny, mem, ew::as_stream(stream), [&](const double* xd, double* yd) {
             ew::kernel_apply(d, xd, yd, permuted, ew::as_stream(stream));
         });
@@ -474,6 +476,7 @@ ew_status ew_kernel_refresh_values(ew_kernel k, ew_csr m, void* stream) {
         auto& d = *k->d;
         const cudaStream_t s = ew::as_stream(stream);
         ew::require(m->d->nrows == d.nrows && m->d->nnz == d.nnz, "refresh: structure mismatch");
+        ew::drop_host_pipeline(d);  // its block layouts hold the old values
         if (d.format && (d.format->kind == ew::FormatData::kEll || d.format->kind == ew::FormatData::kHyb))
             throw ew::Error(EW_UNSUPPORTED, "values-only refresh of ell/hyb kernels is not implemented");
         if (d.csr) {

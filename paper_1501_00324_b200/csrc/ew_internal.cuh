@@ -226,6 +226,34 @@ struct CgWorkspace {
     }
 };
 
+// Host-buffer apply of a large K1 kernel as a copy / compute pipeline: the
+// rows split into B contiguous blocks, each with its own K1 layout (same
+// per-row entry order, so the same row sums); x goes up in B column chunks,
+// block b runs once the chunk holding its largest column has landed, and its
+// y rows go down while later blocks compute (PCIe is full duplex).
+struct HostPipeline {
+    int nblocks = 0;
+    std::vector<int64_t> r0;       // row bounds, nblocks + 1
+    std::vector<int64_t> c0;       // x chunk bounds, nblocks + 1
+    std::vector<int> need;         // per block: last x chunk it reads
+    std::vector<std::shared_ptr<LayoutData>> blocks;
+    DevBuf<double> x, y;
+    cudaStream_t up = nullptr, down = nullptr;
+    std::vector<cudaEvent_t> ev_x, ev_y;
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+    HostPipeline() = default;
+    HostPipeline(const HostPipeline&) = delete;
+    HostPipeline& operator=(const HostPipeline&) = delete;
+    ~HostPipeline() {
+        for (auto e : ev_x) cudaEventDestroy(e);
+        for (auto e : ev_y) cudaEventDestroy(e);
+        if (ev_start) cudaEventDestroy(ev_start);
+        if (ev_done) cudaEventDestroy(ev_done);
+        if (up) cudaStreamDestroy(up);
+        if (down) cudaStreamDestroy(down);
+    }
+};
+
 struct KernelData {
     std::string id;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored_slots = 0;
@@ -237,7 +265,19 @@ struct KernelData {
     DevBuf<int64_t> entry_dst;           // r / rs: original entry -> reordered entry (refresh)
     // CG working sets for cg_solve (0) and cg_solve_permuted (1)
     mutable CgWorkspace cg_ws[2];
+    // host-buffer apply pipeline (built on first use from the layout; dropped
+    // whenever the layout's values change)
+    mutable std::mutex pipe_mu;
+    mutable std::unique_ptr<HostPipeline> pipe;
 };
+
+// y = A x with x, y in host memory through the kernel's HostPipeline; false
+// when the kernel does not qualify (not a large plain K1) or is busy.
+bool kernel_apply_host(const KernelData& k, const double* x, double* y, cudaStream_t s);
+inline void drop_host_pipeline(KernelData& k) {
+    std::lock_guard<std::mutex> g(k.pipe_mu);
+    k.pipe.reset();
+}
 
 std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
                                          cudaStream_t s);

@@ -243,3 +243,36 @@ def test_baseline_formats_long_rows_and_stored_slots(ew, F):
     assert ew.Kernel("ell", a).stored_slots == m.nrows * lens.max()
     assert ew.Kernel("coo", a).stored_slots == m.nnz
     assert ew.Kernel("csr_vector", a).stored_slots == m.nnz
+
+
+def test_host_buffer_pipeline(ew, R, F):
+    """ew_kernel_apply with host buffers on a large K1 (>= 2M nnz) runs as a
+    block pipeline (x up in chunks, y down per row block while later blocks
+    compute): bitwise the device apply, also after a values-only refresh
+    (the pipeline's block layouts are rebuilt from the refreshed layout)."""
+    from oracle.oracle import Csr
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.elasticity_box(30, 30, 30)
+    m = Csr.make(n, n, ro, ci, v)
+    assert m.nnz >= 2_000_000
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    x = np.random.default_rng(5).uniform(-1.0, 1.0, n)
+    import torch
+
+    yd = k.apply(torch.tensor(x, device="cuda")).cpu().numpy()
+    for _ in range(2):
+        assert np.array_equal(bits(k.apply(x)), bits(yd))
+    lay = R.build_k1(m)
+    try:
+        assert np.array_equal(bits(yd), bits(R.spmv_layout(lay, x, scatter=True)))
+    finally:
+        R.free(lay)
+    m2 = Csr.make(n, n, ro, ci, v * 0.5 - 1.0)
+    k.refresh_values(dev_csr(ew, m2))
+    lay = R.build_k1(m2)
+    try:
+        assert np.array_equal(bits(k.apply(x)), bits(R.spmv_layout(lay, x, scatter=True)))
+    finally:
+        R.free(lay)
