@@ -358,7 +358,7 @@ def run_spmv(args, rank, world, local):
                      "frac": round(achieved / hbm, 4) if achieved else None,
                      "traffic": ncu_traffic(f"{args.config}/{args.kernel}") if args.scale == 1.0 else None,
                      "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
-                     "kernel": "k1_kernel" if args.kernel.startswith("k1") else "k2_kernel",
+                     "kernel": ("k1_stream_kernel (grid-stride K1: layout beyond L2, >= 24 slots/row)" if args.config == "c2" else "k1_kernel") if args.kernel.startswith("k1") else "k2_kernel",
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
