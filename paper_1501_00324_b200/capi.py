@@ -268,10 +268,6 @@ class Csr:
         self.nrows, self.ncols, self.nnz = int(nrows), int(ncols), int(nnz)
 
     @staticmethod
-    def from_oracle(m):
-        return Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
-
-    @staticmethod
     def _wrap(h):
         obj = Csr.__new__(Csr)
         obj.h = h
