@@ -328,11 +328,15 @@ def run_spmv(args, rank, world, local):
     for _ in range(2):
         apply(xn, yn)
     barrier(world)
+    calls = []
     t = time.perf_counter()
     for _ in range(k_e2e):
+        t1 = time.perf_counter()
         apply(xn, yn)
+        calls.append(time.perf_counter() - t1)
     e2e_ms = max_over_ranks((time.perf_counter() - t) * 1e3 / k_e2e, world)
     e2e_val = world * eff_bytes / (e2e_ms * 1e-3) / 1e9
+    calls_ms = np.array(calls) * 1e3
 
     out = {
         "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)",
@@ -362,6 +366,8 @@ def run_spmv(args, rank, world, local):
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
+                "call_ms_min_median_max": [round(float(calls_ms.min()), 4), round(float(np.median(calls_ms)), 4),
+                                           round(float(calls_ms.max()), 4)],
                 "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -832,6 +838,8 @@ def main():
     p.add_argument("--iterations", type=int, default=1000)
     p.add_argument("--cpu-cg-iters", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cg-steps", type=int, default=2,
+                   help="spmv workload: also time this many 1000-iteration partitioned CG steps (0: skip)")
     args = p.parse_args()
     args.warmup = max(3, args.warmup)
     if args.config is None:
@@ -858,6 +866,23 @@ def main():
             print(json.dumps(run_suite(args) if args.workload == "suite" else run_alpha(args)), flush=True)
         return
     out = run_spmv(args, rank, world, local) if args.workload == "spmv" else run_cg(args, rank, world, local)
+    if args.workload == "spmv" and args.cg_steps > 0:
+        # BASELINE.json's second metric beside the headline: the partitioned
+        # Jacobi PCG on a config-2-sized elasticity slab per GPU (weak scaling,
+        # the same path at every N, 1000 iterations per step)
+        import gc
+
+        import torch
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        cg_args = argparse.Namespace(**vars(args))
+        cg_args.steps, cg_args.workload = args.cg_steps, "cg"
+        cg = run_cg_dist(cg_args, rank, world, local)
+        if rank == 0:
+            out["cg"] = {key: cg[key] for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup",
+                                                   "ms_per_step", "scaling", "config", "roofline", "e2e",
+                                                   "gpu_launches", "clocks")}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
