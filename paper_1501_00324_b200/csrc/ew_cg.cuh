@@ -415,10 +415,13 @@ static __global__ void __launch_bounds__(kRedBlock) dot_final_kernel(const doubl
 
 // partials / tickets the fused p.q of a plain SpMV grid of `blocks` CTAs needs
 inline size_t dot_final_blocks(int64_t blocks) { return static_cast<size_t>((blocks + kRedBlock - 1) / kRedBlock); }
+// (one partial per SpMV warp: 8 per 256-thread CTA)
 inline size_t dot_partials(int64_t blocks) {
-    return static_cast<size_t>(blocks) + grid_sum_partials(static_cast<int64_t>(dot_final_blocks(blocks)));
+    return static_cast<size_t>(8 * blocks) + grid_sum_partials(static_cast<int64_t>(dot_final_blocks(8 * blocks)));
 }
-inline size_t dot_tickets(int64_t blocks) { return grid_sum_tickets(static_cast<int64_t>(dot_final_blocks(blocks))); }
+inline size_t dot_tickets(int64_t blocks) {
+    return grid_sum_tickets(static_cast<int64_t>(dot_final_blocks(8 * blocks)));
+}
 
 // DIST: sum the all-gathered partition totals in rank order, then decide.
 __device__ __forceinline__ void finalize_body(int what, const double* gathered, int nparts, double tol,

@@ -234,8 +234,10 @@ __global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, double* __rest
         v[0] = __dmul_rn(a.x[t], sum);
     }
     pdl_trigger();
-    cg::block_sum<1>(v);  // fixed tree per CTA
-    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+    // one partial per warp (fixed shuffle tree): no CTA-wide barrier holds
+    // the CTA past its slowest warp
+    const double wsum = cg::warp_sum(v[0]);
+    if ((threadIdx.x & 31) == 0) partials[blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = wsum;
 }
 
 // k1_dot_kernel in the grid-stride form of k1_stream_kernel (large long-row layouts).
@@ -259,8 +261,8 @@ __global__ void __launch_bounds__(256, 8) k1_dot_stream_kernel(K1Args a, double*
         v[0] = __dadd_rn(v[0], __dmul_rn(a.x[t], sum));
     }
     pdl_trigger();
-    cg::block_sum<1>(v);  // fixed tree per CTA
-    if (threadIdx.x == 0) partials[blockIdx.x] = v[0];
+    const double wsum = cg::warp_sum(v[0]);  // one partial per warp
+    if ((threadIdx.x & 31) == 0) partials[blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = wsum;
 }
 
 struct K2Args {
@@ -387,8 +389,10 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
         scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
     }
     launched("k1_dot_kernel");
-    launch_pdl(cg::dot_final_kernel, static_cast<unsigned>(cg::dot_final_blocks(grid)), cg::kRedBlock, s,
-               (const double*)sink.partials, grid, sink.partials + grid, sink.tickets, sink.st, sink.dist, sink.slot);
+    const unsigned nparts = grid * (256 / 32);  // one partial per SpMV warp
+    launch_pdl(cg::dot_final_kernel, static_cast<unsigned>(cg::dot_final_blocks(nparts)), cg::kRedBlock, s,
+               (const double*)sink.partials, nparts, sink.partials + nparts, sink.tickets, sink.st, sink.dist,
+               sink.slot);
     launched("cg::dot_final_kernel");
     return true;
 }
