@@ -154,6 +154,7 @@ struct DistPart {
     DevBuf<cg::State> st;
     // peer transport: mailbox (flags + published dot products), push plan
     DevBuf<uint64_t> mbox;
+    DevBuf<uint64_t> epochs;  // [0] halo exchanges, [1] reductions completed (device counters)
     DevBuf<unsigned> push_ctr;
     DevBuf<PushDesc> descs;  // one per destination peer
     DevBuf<int32_t> srcs;    // peers that send to this partition
@@ -168,7 +169,6 @@ struct DistData {
     bool use_nccl = false;
     bool peer = false;                     // peer transport (in-process or CUDA IPC)
     bool ipc = false;                      // peers live in other processes
-    uint64_t halo_epoch = 0, red_epoch = 0;
     std::vector<void*> ipc_mapped;         // cudaIpcOpenMemHandle mappings to close
     ncclComm_t comm = nullptr;
     std::string kernel_id;
@@ -233,10 +233,11 @@ __device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t e, uint64
 // previous epoch to its own sources (its boundary rows of that epoch are
 // done: this kernel is stream-ordered after them).
 __global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int32_t* __restrict__ idx,
-                            const double* __restrict__ src, int which, uint64_t epoch, uint64_t* const* mboxes,
+                            const double* __restrict__ src, int which, const uint64_t* epochs, uint64_t* const* mboxes,
                             int me, int G, int write_acks, const int32_t* __restrict__ srcs, int nsrc,
                             unsigned* ctr, int64_t total) {
     uint64_t* mine = mboxes[me];
+    const uint64_t epoch = epochs[0] + 1;  // this exchange (halo_wait_kernel advances the counter)
     if (write_acks && blockIdx.x == 0)
         for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch - 1);
     for (int i = threadIdx.x; i < ndesc; i += blockDim.x)
@@ -262,18 +263,26 @@ __global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int
 // In-process peer transport: acks as their own launch (every partition's
 // boundary rows precede every push on the one device).
 __global__ void ack_kernel(uint64_t* const* mboxes, int me, int G, const int32_t* __restrict__ srcs, int nsrc,
-                           uint64_t epoch) {
-    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch);
+                           const uint64_t* epochs) {
+    const uint64_t consumed = epochs[0];  // the last exchange this partition finished reading
+    for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), consumed);
 }
 
 // The ghost tail is complete once every source raised this epoch.
-__global__ void halo_wait_kernel(uint64_t* mine, int G, const int32_t* __restrict__ srcs, int nsrc, uint64_t epoch) {
+// Then advances the partition's halo epoch counter (launched once per
+// exchange, sources or not).
+__global__ void halo_wait_kernel(uint64_t* mine, int G, const int32_t* __restrict__ srcs, int nsrc,
+                                 uint64_t* epochs) {
+    const uint64_t epoch = epochs[0] + 1;
     for (int i = threadIdx.x; i < nsrc; i += blockDim.x) spin_until(mine + Mbox::halo(srcs[i]), epoch, mine + Mbox::err(G));
+    __syncthreads();
+    if (threadIdx.x == 0) epochs[0] = epoch;
 }
 
 // Reduction, step 1: this partition's totals (State::loc) into slot `me` of
 // every partition's mailbox (its own included), then the flag.
-__global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int me, int G, uint64_t epoch) {
+__global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int me, int G, const uint64_t* epochs) {
+    const uint64_t epoch = epochs[1] + 1;  // this reduction (the collect kernel advances the counter)
     const int g = threadIdx.x;
     if (g >= G) return;
     uint64_t* mb = mboxes[g];
@@ -286,19 +295,8 @@ __global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int
 
 // Reduction, step 2: wait for every partition's totals, copy them to
 // `gathered` in rank order (then cg::finalize_kernel sums them).
-__global__ void collect_kernel(uint64_t* mine, int G, uint64_t epoch, double* gathered) {
-    const int g = threadIdx.x;
-    if (g >= G) return;
-    spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
-    const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
-    gathered[2 * g] = ld_relaxed_sys(v);
-    gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
-}
-
-// collect_kernel and cg::finalize_kernel in one launch: thread g waits for
-// partition g's totals, thread 0 sums them in rank order and decides.
-__global__ void collect_finalize_kernel(uint64_t* mine, int G, uint64_t epoch, double* gathered, int what,
-                                        double tol, double divergence, cg::State* st, double* hist) {
+__global__ void collect_kernel(uint64_t* mine, int G, uint64_t* epochs, double* gathered) {
+    const uint64_t epoch = epochs[1] + 1;
     const int g = threadIdx.x;
     if (g < G) {
         spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
@@ -307,7 +305,26 @@ __global__ void collect_finalize_kernel(uint64_t* mine, int G, uint64_t epoch, d
         gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) cg::finalize_body(what, gathered, G, tol, divergence, st, hist);
+    if (threadIdx.x == 0) epochs[1] = epoch;
+}
+
+// collect_kernel and cg::finalize_kernel in one launch: thread g waits for
+// partition g's totals, thread 0 sums them in rank order and decides.
+__global__ void collect_finalize_kernel(uint64_t* mine, int G, uint64_t* epochs, double* gathered, int what,
+                                        double tol, double divergence, cg::State* st, double* hist) {
+    const uint64_t epoch = epochs[1] + 1;
+    const int g = threadIdx.x;
+    if (g < G) {
+        spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
+        const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
+        gathered[2 * g] = ld_relaxed_sys(v);
+        gathered[2 * g + 1] = ld_relaxed_sys(v + 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        epochs[1] = epoch;
+        cg::finalize_body(what, gathered, G, tol, divergence, st, hist);
+    }
 }
 
 // Ghost columns of a row block [r0, r1) given with global column ids:
@@ -432,12 +449,11 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
 using PartPtrs = std::vector<const double*>;
 
 void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream_t s, const PartPtrs* src = nullptr) {
-    const uint64_t e = ++D.halo_epoch;
     const int32_t G = D.nparts;
     if (!D.ipc) {
         for (auto& P : D.parts) {
             if (!P->nsrc) continue;
-            ack_kernel<<<1, 32, 0, s>>>(P->mboxes.get(), P->part, G, P->srcs.get(), P->nsrc, e - 1);
+            ack_kernel<<<1, 32, 0, s>>>(P->mboxes.get(), P->part, G, P->srcs.get(), P->nsrc, P->epochs.get());
             launched("ack_kernel");
         }
     }
@@ -447,7 +463,7 @@ void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream
         if (!total && (!D.ipc || !P->nsrc)) continue;
         const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(total), 148 * 4));
         const double* from = src ? (*src)[i] : ((*P).*ext).get();
-        push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), from, which, e,
+        push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), from, which, P->epochs.get(),
                                             P->mboxes.get(), P->part, G, D.ipc ? 1 : 0, P->srcs.get(), P->nsrc,
                                             P->push_ctr.get(), total);
         launched("push_kernel");
@@ -458,8 +474,7 @@ void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream
 // epoch has landed.
 void peer_wait(DistData& D, cudaStream_t s) {
     for (auto& P : D.parts) {
-        if (!P->nsrc) continue;
-        halo_wait_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, P->srcs.get(), P->nsrc, D.halo_epoch);
+        halo_wait_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, P->srcs.get(), P->nsrc, P->epochs.get());
         launched("halo_wait_kernel");
     }
 }
@@ -514,13 +529,12 @@ void halo(DistData& D, DevBuf<double> DistPart::*ext, cudaStream_t s, const Part
 // Every partition's State::loc[0..1] into every partition's `gathered`.
 void allgather(DistData& D, cudaStream_t s) {
     if (D.peer) {
-        const uint64_t e = ++D.red_epoch;
         for (auto& P : D.parts) {
-            publish_kernel<<<1, 32, 0, s>>>(P->st.get(), P->mboxes.get(), P->part, D.nparts, e);
+            publish_kernel<<<1, 32, 0, s>>>(P->st.get(), P->mboxes.get(), P->part, D.nparts, P->epochs.get());
             launched("publish_kernel");
         }
         for (auto& P : D.parts) {
-            collect_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, e, P->gathered.get());
+            collect_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, P->epochs.get(), P->gathered.get());
             launched("collect_kernel");
         }
         return;
@@ -552,13 +566,12 @@ void reduce_finalize(DistData& D, int what, const ew_cg_config& cfg, cudaStream_
         finalize(D, what, cfg, s);
         return;
     }
-    const uint64_t e = ++D.red_epoch;
     for (auto& P : D.parts) {
-        publish_kernel<<<1, 32, 0, s>>>(P->st.get(), P->mboxes.get(), P->part, D.nparts, e);
+        publish_kernel<<<1, 32, 0, s>>>(P->st.get(), P->mboxes.get(), P->part, D.nparts, P->epochs.get());
         launched("publish_kernel");
     }
     for (auto& P : D.parts) {
-        collect_finalize_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, e, P->gathered.get(), what,
+        collect_finalize_kernel<<<1, 32, 0, s>>>(P->mbox.get(), D.nparts, P->epochs.get(), P->gathered.get(), what,
                                                  cfg.rel_tolerance, cfg.divergence_limit, P->st.get(),
                                                  P->hist.get());
         launched("collect_finalize_kernel");
@@ -675,6 +688,8 @@ void peer_plan(DistPart& P, int32_t G, const std::vector<double*>& peer_p, const
 
 void alloc_mailbox(DistPart& P, int32_t G, cudaStream_t s) {
     P.mbox.alloc(Mbox::words(G));
+    P.epochs.alloc(2);
+    EW_CUDA_CHECK(cudaMemsetAsync(P.epochs.get(), 0, P.epochs.bytes(), s));
     P.push_ctr.alloc(1);
     EW_CUDA_CHECK(cudaMemsetAsync(P.mbox.get(), 0, P.mbox.bytes(), s));
     EW_CUDA_CHECK(cudaMemsetAsync(P.push_ctr.get(), 0, P.push_ctr.bytes(), s));
