@@ -177,7 +177,16 @@ struct DistData {
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     void* hst = nullptr;                   // pinned cg::State[2] for CG polling
     cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+    // CG graph of one refresh block (device transports; NCCL runs host-driven)
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t per_block = 0;
+    double g_tol = 0.0, g_div = 0.0;
+    int64_t g_interval = -1, g_hist = -1;
+    int g_jacobi = -1;
     ~DistData() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (cap) cudaStreamDestroy(cap);
         if (hst) cudaFreeHost(hst);
         for (auto e : poll_ev)
             if (e) cudaEventDestroy(e);
@@ -1084,43 +1093,92 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
     auto cleanup = [] {};
     cg::State h{};
     try {
-        int64_t it = 1;
-        int batch = 8, j = 0;
-        while (it <= cfg.max_iterations) {
-            const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
-            for (; it <= last; ++it) {
-                spmv_exchange(D, &DistPart::p_ext, s, true, true);
-                reduce_finalize(D, cg::kPq, cfg, s);
-                const bool refresh = cfg.recompute_interval > 0 && it % cfg.recompute_interval == 0;
-                for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
-                    if (mode < 0) break;
-                    if (mode == 2) spmv_exchange(D, &DistPart::x_ext, s, true, false);
-                    for (auto& P : D.parts) {
-                        cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock,
-                                                                    P->nloc),
-                                                  cg::kRedBlock, 0, s>>>(
-                            mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
-                            P->nloc, jacobi, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(),
-                            P->st.get(), P->hist.get());
-                        launched("cg::update_kernel<dist>");
-                    }
-                }
-                reduce_finalize(D, cg::kUpdate, cfg, s);
+        // one CG iteration on stream t (cg.cpp:69-101); k only selects the
+        // launch pattern (refresh), the kernels count iterations on the device
+        auto iteration = [&](int64_t k, cudaStream_t t) {
+            spmv_exchange(D, &DistPart::p_ext, t, true, true);
+            reduce_finalize(D, cg::kPq, cfg, t);
+            const bool refresh = cfg.recompute_interval > 0 && k % cfg.recompute_interval == 0;
+            for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
+                if (mode < 0) break;
+                if (mode == 2) spmv_exchange(D, &DistPart::x_ext, t, true, false);
                 for (auto& P : D.parts) {
-                    cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, s>>>(P->p_ext.get(), P->r.get(), P->diag.get(),
-                                                                          P->nloc, jacobi, P->st.get());
-                    launched("cg::p_kernel");
+                    cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock, P->nloc),
+                                              cg::kRedBlock, 0, t>>>(
+                        mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
+                        P->nloc, jacobi, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(), P->st.get(),
+                        P->hist.get());
+                    launched("cg::update_kernel<dist>");
                 }
             }
+            reduce_finalize(D, cg::kUpdate, cfg, t);
+            for (auto& P : D.parts) {
+                cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, t>>>(
+                    P->p_ext.get(), P->r.get(), P->diag.get(), P->nloc, jacobi, P->st.get());
+                launched("cg::p_kernel");
+            }
+        };
+        // every rank launches the same blocks and stops on the same polled
+        // state (identical decisions everywhere), so the exchanges pair up
+        int j = 0;
+        auto poll = [&]() -> bool {
             const int slot = j & 1;
             EW_CUDA_CHECK(cudaMemcpyAsync(&hst[slot], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
             EW_CUDA_CHECK(cudaEventRecord(ev[slot], s));
+            bool stop = false;
             if (j > 0) {
                 EW_CUDA_CHECK(cudaEventSynchronize(ev[slot ^ 1]));
-                if (hst[slot ^ 1].done) break;
+                stop = hst[slot ^ 1].done != 0;
             }
             ++j;
-            batch = std::min(batch * 2, 64);
+            return stop;
+        };
+        const int64_t interval = cfg.recompute_interval;
+        if (!D.use_nccl && cfg.max_iterations > 0) {
+            // device transports: one CUDA graph of a refresh block, replayed
+            // (the comm stream joins the capture through its events)
+            const int64_t B = interval > 0 ? interval : 32;
+            const int64_t hsize = static_cast<int64_t>(P0.hist.size());
+            const bool same = D.exec && D.g_tol == cfg.rel_tolerance && D.g_div == cfg.divergence_limit &&
+                              D.g_interval == interval && D.g_jacobi == jacobi && D.g_hist == hsize;
+            if (!same) {
+                if (D.exec) cudaGraphExecDestroy(D.exec);
+                D.exec = nullptr;
+                if (!D.cap) EW_CUDA_CHECK(cudaStreamCreateWithFlags(&D.cap, cudaStreamNonBlocking));
+                const int64_t before = g_launches.load();
+                cudaGraph_t graph = nullptr;
+                EW_CUDA_CHECK(cudaStreamBeginCapture(D.cap, cudaStreamCaptureModeThreadLocal));
+                try {
+                    for (int64_t k = 1; k <= B; ++k) iteration(k, D.cap);
+                } catch (...) {
+                    cudaStreamEndCapture(D.cap, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                EW_CUDA_CHECK(cudaStreamEndCapture(D.cap, &graph));
+                const cudaError_t e = cudaGraphInstantiate(&D.exec, graph, 0);
+                cudaGraphDestroy(graph);
+                EW_CUDA_CHECK(e);
+                D.per_block = g_launches.load() - before;
+                g_launches.fetch_sub(D.per_block, std::memory_order_relaxed);  // counted per replay below
+                D.g_tol = cfg.rel_tolerance, D.g_div = cfg.divergence_limit, D.g_interval = interval;
+                D.g_jacobi = jacobi, D.g_hist = hsize;
+            }
+            const int64_t blocks = (cfg.max_iterations + B - 1) / B;
+            for (int64_t blk = 0; blk < blocks; ++blk) {
+                EW_CUDA_CHECK(cudaGraphLaunch(D.exec, s));
+                g_launches.fetch_add(D.per_block, std::memory_order_relaxed);
+                if (poll()) break;
+            }
+        } else {
+            int64_t it = 1;
+            int batch = 8;
+            while (it <= cfg.max_iterations) {
+                const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
+                for (; it <= last; ++it) iteration(it, s);
+                if (poll()) break;
+                batch = std::min(batch * 2, 64);
+            }
         }
         EW_CUDA_CHECK(cudaMemcpyAsync(&hst[0], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
         EW_CUDA_CHECK(cudaStreamSynchronize(s));

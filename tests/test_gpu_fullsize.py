@@ -81,9 +81,10 @@ def test_config4_k1rs_both_row_orders(ew, R, c4):
 def test_config4_cg_properties(ew, R, c4):
     """Jacobi PCG on config 4 to tol 1e-8 (b = A 1): converged, the true
     residual of the returned solution is at the tolerance, and the reference
-    and locality row orders take the same number of iterations within 1%
-    (~2,460 iterations; the dot products round differently and the last
-    hundreds of iterations creep along a plateau near 1e-8)."""
+    and locality row orders reach 1e-6 within 1% of the same iteration. (The
+    total, ~2,450 iterations, varies by a few percent: the dot products round
+    differently and the last hundreds of iterations creep along a plateau
+    near 1e-8, where the stopping iteration is rounding-sensitive.)"""
     a = dev(ew, c4)
     diag = a.extract_diagonal()
     b = a.spmv(np.ones(c4.ncols))
@@ -99,8 +100,10 @@ def test_config4_cg_properties(ew, R, c4):
         assert res.residual_history[-1] <= 1e-8
         assert np.all(np.isfinite(res.residual_history))
         runs[order] = res
+    first = {o: int(np.argmax(r.residual_history <= 1e-6)) for o, r in runs.items()}
+    assert abs(first["reference"] - first["locality"]) <= max(1, first["reference"] // 100), first
     its = runs["reference"].iterations
-    assert abs(its - runs["locality"].iterations) <= max(1, its // 100)
+    assert abs(its - runs["locality"].iterations) <= max(1, its // 20)
     assert np.allclose(runs["reference"].solution, runs["locality"].solution, rtol=1e-6, atol=1e-6)
 
 
