@@ -142,8 +142,17 @@ def dist_init(n_gpus):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("EW_BENCH_SHARE_GPU"):
+            # functional runs of the N > 1 path on a box with fewer GPUs than
+            # ranks (ranks share devices; the IPC transport works between
+            # processes on one device; gloo for the setup allgather). Not a
+            # measurement.
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -162,7 +171,7 @@ def max_over_ranks(v, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -173,7 +182,7 @@ def sum_over_ranks(vals, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t)
     return [float(x) for x in t.tolist()]
 
