@@ -234,3 +234,32 @@ def test_ipc_transport_two_processes(ew):
     for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
         assert ok_spmv, (rank, it)
         assert ok_cg, (rank, it, ref_it)
+
+
+def test_bench_two_ranks_functional(tmp_path):
+    """bench.py's N > 1 path (partitioned SpMV + CG, IPC transport) under
+    torchrun with two ranks sharing this GPU: runs end to end and prints one
+    JSON line with both metrics (a functional check, not a measurement)."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, EW_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3",
+           "--scale", "0.25", "--iterations", "60", "--cg-steps", "1", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["transport"] == "ipc"
+    assert line["cg"]["n_gpus"] == 2 and line["cg"]["value"] > 0
+    assert line["cg"]["config"]["final_residual"] < 1.0
