@@ -14,7 +14,10 @@ void retain_pool() {
     if (done_mask.load(std::memory_order_relaxed) & bit) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = ~uint64_t{0};
+        // keep up to 8 GB of freed scratch (every per-call buffer of the
+        // hot paths); beyond that, transient setup buffers (e.g. the int64
+        // column staging of a 100M-row upload) go back to the driver
+        uint64_t keep = uint64_t{8} << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     done_mask.fetch_or(bit, std::memory_order_relaxed);

@@ -107,9 +107,10 @@ class DevBuf {
     size_t n_ = 0;
 };
 
-// Keeps freed scratch in the current device's default memory pool instead of
-// returning it to the driver at every synchronisation (the default release
-// threshold is 0: each call would re-map its scratch, ~0.1 ms).
+// Keeps freed scratch (up to 8 GB) in the current device's default memory
+// pool instead of returning it to the driver at every synchronisation (the
+// default release threshold is 0: each call would re-map its scratch,
+// ~0.1 ms).
 void retain_pool();
 
 // Stream-ordered scratch (cudaMallocAsync from the device's default pool).
