@@ -32,9 +32,9 @@ CgOutputs cg_run(const CgOperator& op, CgWorkspace& w, const double* b_in, const
     const int jacobi = cfg.jacobi ? 1 : 0;
     // CG reductions use 2 x kRedGridMax partials; the SpMV-fused p.q one per
     // SpMV CTA plus its final two-level sum
-    const int64_t spmv_blocks = (n + 255) / 256;
+    const int64_t spmv_blocks = (std::max<int64_t>(n, op.spmv_threads()) + 255) / 256;
     const size_t npart = std::max<size_t>(2 * cg::kRedGridMax, cg::dot_partials(spmv_blocks));
-    if (w.n != n) {
+    if (w.n != n || w.partials.size() < npart) {
         w.r.alloc(n), w.p.alloc(n), w.q.alloc(n), w.x.alloc(n), w.b.alloc(n), w.diag.alloc(n);
         w.partials.alloc(npart);
         w.tickets.alloc(std::max<size_t>(1, cg::dot_tickets(spmv_blocks)));

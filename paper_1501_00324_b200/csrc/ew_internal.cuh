@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <memory>
@@ -392,6 +393,8 @@ struct CgOperator {
     virtual int64_t size() const = 0;
     // a working set kept between solves with this operator (nullable)
     virtual CgWorkspace* workspace() const { return nullptr; }
+    // threads of the operator's SpMV launch (sizes the fused p.q partials)
+    virtual int64_t spmv_threads() const { return size(); }
 };
 struct KernelOperator final : CgOperator {
     const KernelData& k;
@@ -405,6 +408,10 @@ struct KernelOperator final : CgOperator {
     }
     int64_t size() const override { return k.nrows == k.ncols ? k.nrows : -1; }
     CgWorkspace* workspace() const override { return &k.cg_ws[permuted ? 1 : 0]; }
+    int64_t spmv_threads() const override {
+        if (k.layout && k.layout->kind == EW_LAYOUT_K2) return std::max(k.nrows, k.layout->nwarps * k.layout->ws);
+        return k.nrows;
+    }
 };
 // Device CG. b, diag, x are device pointers in the operator's numbering.
 CgOutputs cg_device(const CgOperator& op, const double* b, const double* diag, int64_t n,

@@ -285,8 +285,10 @@ struct K2Args {
 // K2 / K2r / K2rs (warp_spmv.cpp:62-126) for warp_size <= 32: thread t is lane
 // t % ws of layout warp t / ws; `reduction` lanes share a row, each summing a
 // contiguous chunk of maxrows slots, then the ascending-stride tree.
-template <bool SORTED, bool SCATTER>
-__global__ void __launch_bounds__(256) k2_kernel(K2Args a) {
+// DOT (the CG's fused p.q): each row's leader adds x[target] * y[target];
+// one partial per hardware warp, summed by cg::dot_final_kernel.
+template <bool SORTED, bool SCATTER, bool DOT = false>
+__global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ partials) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t w = t >> a.ws_log2;
     const int32_t lane = static_cast<int32_t>(t & (a.ws - 1));
@@ -314,8 +316,13 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a) {
         const double o = __shfl_down_sync(0xffffffffu, sum, st);
         if (st < red && (tl & (2 * st - 1)) == 0) sum = __dadd_rn(sum, o);
     }
-    if (leader) a.y[SCATTER ? a.fwd[pos] : pos] = sum;
+    const int64_t target = SCATTER && leader ? a.fwd[pos] : pos;
+    if (leader) a.y[target] = sum;
     pdl_trigger();
+    if (DOT) {
+        const double part = cg::warp_sum(leader ? __dmul_rn(a.x[target], sum) : 0.0);
+        if ((threadIdx.x & 31) == 0) partials[blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)] = part;
+    }
 }
 
 // K2 for warp_size in (32, 1024]: one CTA of ws threads per layout warp, the
@@ -361,7 +368,7 @@ template <bool SORTED, bool SCATTER>
 void launch_k2(const K2Args& a, cudaStream_t s) {
     if (a.nwarps == 0) return;
     if (a.ws <= 32) {
-        launch_pdl(k2_kernel<SORTED, SCATTER>, grid_for(a.nwarps * a.ws), kBlock, s, a);
+        launch_pdl(k2_kernel<SORTED, SCATTER>, grid_for(a.nwarps * a.ws), kBlock, s, a, (double*)nullptr);
     } else {
         k2_wide_kernel<SORTED, SCATTER><<<static_cast<unsigned>(a.nwarps), a.ws, a.ws * sizeof(double), s>>>(a);
     }
@@ -372,7 +379,29 @@ void launch_k2(const K2Args& a, cudaStream_t s) {
 
 bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
                      const int* done, const DotSink& sink) {
-    if (l.kind != EW_LAYOUT_K1 || l.row_major || l.nrows == 0) return false;
+    if (l.row_major || l.nrows == 0) return false;
+    if (l.kind == EW_LAYOUT_K2) {
+        // K2 with ws <= 32 and every row covered (a built, not imported, layout)
+        if (l.ws > 32 || l.imported || l.nwarps == 0) return false;
+        K2Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.reduction.get(),
+                 l.rows_offset_warp.get(), l.rows_in_warp.get(), l.slen.get(), l.fwd.get(), x, y, done,
+                 l.nwarps, l.n_active, l.ws, l.ws_log2};
+        const unsigned grid = grid_for(l.nwarps * l.ws);
+        if (cg::dot_partials(grid) > sink.capacity) return false;
+        auto go = [&](auto kernel) { launch_pdl(kernel, grid, kBlock, s, a, sink.partials); };
+        if (l.sorted)
+            scatter ? go(k2_kernel<true, true, true>) : go(k2_kernel<true, false, true>);
+        else
+            scatter ? go(k2_kernel<false, true, true>) : go(k2_kernel<false, false, true>);
+        launched("k2_kernel");
+        const unsigned nparts = grid * (kBlock / 32);
+        launch_pdl(cg::dot_final_kernel, static_cast<unsigned>(cg::dot_final_blocks(nparts)), cg::kRedBlock, s,
+                   (const double*)sink.partials, nparts, sink.partials + nparts, sink.tickets, sink.st, sink.dist,
+                   sink.slot);
+        launched("cg::dot_final_kernel");
+        return true;
+    }
+    if (l.kind != EW_LAYOUT_K1) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
     const unsigned grid = grid_for(l.nrows);
