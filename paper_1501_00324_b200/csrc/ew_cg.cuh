@@ -309,6 +309,27 @@ __global__ void __launch_bounds__(kRedBlock) pq_kernel(const double* __restrict_
     finish<DIST, 1>(v, partials, st, [&](const double (&t)[1]) { decide_pq(st, t[0]); });
 }
 
+// L2 eviction hints for the vector kernels: data the next kernel reads again
+// (r, diag, p: the p update) is kept, data it does not (x, q) goes first.
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // mode 0: x += alpha p, r -= alpha q, then r.r, r.z   (cg.cpp:78-81, 88-99)
 // mode 1: x += alpha p only (refresh iteration, first half)
 // mode 2: r = b - A x (A x in q), then r.r, r.z       (cg.cpp:82-86)
@@ -322,6 +343,7 @@ __global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* 
     pdl_wait();
     if (st->done) return;
     const double alpha = st->alpha;
+    const uint64_t first = l2_policy_first(), last = l2_policy_last();
     double v[2] = {0.0, 0.0};
     int bad = 0;
     EW_ROUNDS_U(i0, S, n, kUpdU) {
@@ -330,21 +352,21 @@ __global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* 
         for (int u = 0; u < kUpdU; ++u) {
             const int64_t i = i0 + u * S;
             const bool ok = i < n;
-            xv[u] = ok && mode != 2 ? x[i] : 0.0;
-            pv[u] = ok && mode != 2 ? p[i] : 0.0;
-            qv[u] = ok && mode != 1 ? q[i] : 0.0;
+            xv[u] = ok && mode != 2 ? ld_hint(x + i, first) : 0.0;
+            pv[u] = ok && mode != 2 ? ld_hint(p + i, last) : 0.0;
+            qv[u] = ok && mode != 1 ? ld_hint(q + i, first) : 0.0;
             rv[u] = ok && mode != 1 ? (mode == 0 ? r[i] : b[i]) : 0.0;
-            dv[u] = ok && mode != 1 && jacobi ? diag[i] : 1.0;
+            dv[u] = ok && mode != 1 && jacobi ? ld_hint(diag + i, last) : 1.0;
         }
 #pragma unroll
         for (int u = 0; u < kUpdU; ++u) {
             const int64_t i = i0 + u * S;
             if (i >= n) continue;
-            if (mode != 2) x[i] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+            if (mode != 2) st_hint(x + i, __dadd_rn(xv[u], __dmul_rn(alpha, pv[u])), first);
             if (mode == 1) continue;
             // mode 0: r - alpha q; mode 2: b - Ax (rv holds b)
             const double ri = mode == 0 ? __dsub_rn(rv[u], __dmul_rn(alpha, qv[u])) : __dsub_rn(rv[u], qv[u]);
-            r[i] = ri;
+            st_hint(r + i, ri, last);
             bad |= !isfinite(ri);
             const double zi = jacobi ? __ddiv_rn(ri, dv[u]) : ri;
             v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
