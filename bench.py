@@ -821,7 +821,8 @@ def run_reference(args, rank, world):
         return {"impl": "reference", "metric": "CG iterations/s", "value": round(rate, 3), "unit": "it/s",
                 "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": True,
                 "config": {"workload": CONFIGS[args.config]["name"]},
-                "cpu_baseline": {"kind": "reference", "cores": cores, "value": round(rate, 3),
+                "cpu_baseline": {"kind": "reference", "cores": cores, "host_cores": os.cpu_count(),
+                                 "value": round(rate, 3),
                                  "sample": f"{its} iterations cg_solve(csr_ref)"},
                 "e2e": {"value": round(rate, 3), "unit": "it/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -833,7 +834,8 @@ def run_reference(args, rank, world):
             "unit": "GB/s", "n_gpus": world, "steps": calls, "warmup": args.warmup, "ms_per_step": round(med * 1e3, 3),
             "higher_is_better": True, "dtype": "f64",
             "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel},
-            "cpu_baseline": {"kind": "reference", "cores": cores, "value": round(val, 3), "unit": "GB/s",
+            "cpu_baseline": {"kind": "reference", "cores": cores, "host_cores": os.cpu_count(),
+                             "value": round(val, 3), "unit": "GB/s",
                              "sample": f"median of {calls} prepare_kernel('{args.kernel}').apply calls, full matrix "
                                        "(oracle/_ref compiled from the reference sources; single-threaded "
                                        "by construction)"},
