@@ -156,3 +156,35 @@ def test_recompute_interval_and_long_run(ew, R, F):
         assert res.iterations == 300 and not res.converged
         assert res.spmv_calls == ref.spmv_calls
         assert_history(res.residual_history, ref.residual_history)
+
+
+def test_no_device_memory_growth(ew, F):
+    """Prepared kernels own their CG working sets and host-apply pipelines:
+    creating, using and dropping them repeatedly leaves device memory flat."""
+    import gc
+
+    import torch
+
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.elasticity_box(30, 30, 30)  # large enough for the host pipeline
+    a = ew.Csr(n, n, ro, ci, v)
+    diag = a.extract_diagonal()
+    b = a.spmv(np.ones(n))
+    x = np.linspace(0.1, 1.0, n)
+
+    def cycle():
+        for kid in ("k1", "k1rs"):
+            k = ew.Kernel(kid, a)
+            k.cg_solve(b, diag, max_iterations=60, tol=1e-300, permuted=k.has_perm)
+            k.apply(x)
+            del k
+        gc.collect()
+        torch.cuda.synchronize()
+
+    cycle()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        cycle()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20
