@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= a.nrows || (a.done && *a.done)) return;
     const uint64_t pol = evict_first_policy();
+    // the scatter target is loaded with the metadata, not after the row sum
+    const int64_t target = SCATTER ? a.fwd[p] : p;
     double sum = 0.0;
     const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
     if (active) {
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
         sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, ROW_MAJOR ? 1 : a.ws, mx, pol)
                       : lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
     }
-    a.y[SCATTER ? a.fwd[p] : p] = sum;
+    a.y[target] = sum;
     pdl_trigger();
 }
 
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ 
     double sum = 0.0;
     int32_t red = 1, tl = 0;
     bool leader = false;
-    int64_t pos = 0;
+    int64_t pos = 0, target = 0;
     if (w < a.nwarps) {
         red = a.reduction[w];
         const int32_t rl = __ffs(red) - 1;
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ 
         if (r < a.rows_in_warp[w]) {
             pos = int64_t(a.rows_offset_warp[w]) + r;
             leader = tl == 0;
+            if (SCATTER && leader) target = a.fwd[pos];  // with the metadata, not after the sum
             const bool active = SORTED ? pos < a.n_active : a.slen[pos] > 0;
             if (active) sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
         }
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ 
         const double o = __shfl_down_sync(0xffffffffu, sum, st);
         if (st < red && (tl & (2 * st - 1)) == 0) sum = __dadd_rn(sum, o);
     }
-    const int64_t target = SCATTER && leader ? a.fwd[pos] : pos;
+    if (!SCATTER) target = pos;
     if (leader) a.y[target] = sum;
     pdl_trigger();
     if (DOT) {
