@@ -170,6 +170,11 @@ const char* ew_kernel_id(int32_t i);
 int32_t ew_kernel_id_supported(const char* id);
 /* Count of this library's kernel launches since load (all streams). */
 int64_t ew_launch_count(void);
+/* Benchmark helper, stream-ordered L2 flush: reads `bytes` of the device
+ * buffer `buf` (pass >= 2x the L2 size) with an L2 evict_last policy, so it
+ * also displaces the lines the SpMV kernels tag evict_last (the x gathers),
+ * which a plain read of a large buffer would not. */
+ew_status ew_l2_flush(const void* buf, int64_t bytes, void* stream);
 
 /* ---- matrices (csr.hpp / csr.cpp) --------------------------------------- */
 /* Upload + validate_csr (csr.cpp:57-73) on the device. Row offsets and

@@ -112,6 +112,7 @@ _SIGS = {
     "ew_kernel_id": (C.c_char_p, [C.c_int32]),
     "ew_kernel_id_supported": (C.c_int32, [C.c_char_p]),
     "ew_launch_count": (C.c_int64, []),
+    "ew_l2_flush": (C.c_int, [_vp, C.c_int64, _vp]),
     "ew_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_int, C.c_int32,
                                 _vp, C.POINTER(_vp)]),
     "ew_csr_destroy": (C.c_int, [_vp]),
@@ -220,6 +221,12 @@ def kernel_ids():
 
 def launch_count():
     return int(lib().ew_launch_count())
+
+
+def l2_flush(buf, stream=None):
+    """Stream-ordered L2 flush through a device tensor (>= 2x L2) read with an
+    evict_last policy (ew_l2_flush)."""
+    check(lib().ew_l2_flush(_ptr(buf), buf.numel() * buf.element_size(), _stream_ptr(stream)))
 
 
 # --------------------------------------------------------------------------
