@@ -216,6 +216,26 @@ def reference_spmv_rate(n, nc, ro, ci, v, kernel="k1", budget_s=15.0, max_calls=
     return med, len(times), t_prep
 
 
+def port_spmv_rate_mt(n, nc, ro, ci, v, threads, budget_s=8.0, max_calls=50):
+    """The oracle's row-parallel (pthreads) CSR SpMV port on `threads` host
+    threads: a multi-core CPU comparison beside the single-threaded
+    reference (same row sums)."""
+    from oracle.oracle import Csr, Restatement
+
+    R = Restatement()
+    m = Csr.make(n, nc, ro, ci, v)
+    x = np.random.default_rng(1).uniform(0.1, 1.0, nc)
+    y = np.empty(n)
+    R.spmv_csr_mt(m, x, threads, y)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_calls and (time.perf_counter() - t_start) < budget_s:
+        t = time.perf_counter()
+        R.spmv_csr_mt(m, x, threads, y)
+        times.append(time.perf_counter() - t)
+    return float(np.median(times)), len(times)
+
+
 def reference_cg_rate(n, nc, ro, ci, v, iters):
     from oracle.oracle import Csr, Reference
 
@@ -401,6 +421,13 @@ def run_spmv(args, rank, world, local):
                                "sample": f"{what}, median of {calls} prepare_kernel('"
                                          f"{args.kernel}').apply calls (oracle/_ref, 1 thread); "
                                          f"CPU layout build {t_prep:.1f}s"}
+        threads = os.cpu_count() or 1
+        mt, mcalls = port_spmv_rate_mt(rows, nc, ro[:rows + 1], ci[:rnnz], v[:rnnz], threads)
+        out["cpu_baseline_multicore"] = {"value": round(20 * rnnz / mt / 1e9, 3), "unit": "GB/s", "cores": threads,
+                                         "kind": "port",
+                                         "sample": f"{what}, median of {mcalls} row-parallel CSR SpMV calls of the "
+                                                   f"oracle's pthreads port on all {threads} host threads (the "
+                                                   "reference itself has no threading)"}
     return out
 
 

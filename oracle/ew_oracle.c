@@ -2,9 +2,11 @@
  * ONLY -- see ew_oracle.h for what pins it. Compiled with -ffp-contract=off so
  * every a*b+c rounds twice, as the reference's default (non -march=native)
  * build does. File:line citations are into /root/reference/proj. */
+#define _POSIX_C_SOURCE 200809L
 #include "ew_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -19,6 +21,42 @@ int ewo_spmv_csr(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t*
         for (int64_t k = ro[r]; k < ro[r + 1]; ++k) sum += v[k] * x[ci[k]];
         y[r] = sum;
     }
+    return 0;
+}
+
+/* The same row sums on `threads` POSIX threads (contiguous row ranges): a
+ * clearly-labelled multi-core PORT for the bench's CPU comparison (the
+ * reference itself is single-threaded). Bitwise equal to ewo_spmv_csr. */
+typedef struct {
+    int64_t r0, r1;
+    const int64_t *ro, *ci;
+    const double *v, *x;
+    double* y;
+} ewo_mt_job;
+
+static void* ewo_mt_rows(void* arg) {
+    const ewo_mt_job* j = (const ewo_mt_job*)arg;
+    for (int64_t r = j->r0; r < j->r1; ++r) {
+        double sum = 0.0;
+        for (int64_t k = j->ro[r]; k < j->ro[r + 1]; ++k) sum += j->v[k] * j->x[j->ci[k]];
+        j->y[r] = sum;
+    }
+    return NULL;
+}
+
+int ewo_spmv_csr_mt(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
+                    const double* v, const double* x, double* y, int threads) {
+    (void)ncols;
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    ewo_mt_job job[256];
+    for (int t = 0; t < threads; ++t) {
+        job[t] = (ewo_mt_job){nrows * t / threads, nrows * (t + 1) / threads, ro, ci, v, x, y};
+        if (t > 0 && pthread_create(&tid[t], NULL, ewo_mt_rows, &job[t]) != 0) return -1;
+    }
+    ewo_mt_rows(&job[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
     return 0;
 }
 

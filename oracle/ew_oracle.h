@@ -27,6 +27,9 @@ extern "C" {
 /* Return codes: 0 ok, 1 invalid argument (std::invalid_argument),
  * 2 CG divergence (CgDivergenceError). */
 
+/* row-parallel (pthreads) port of spmv_csr_reference (bench CPU comparison only) */
+int ewo_spmv_csr_mt(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
+                    const double* v, const double* x, double* y, int threads);
 /* csr.cpp:75-86 spmv_csr_reference */
 int ewo_spmv_csr(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_t* ci,
                  const double* v, const double* x, double* y);

@@ -170,6 +170,14 @@ class Restatement:
                               _ip(m.col_indices), _fp(m.values), _fp(x), _fp(y))
         return y
 
+    def spmv_csr_mt(self, m: Csr, x, threads, y=None):
+        """Row-parallel pthreads port (bench CPU comparison only)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty(m.nrows, np.float64) if y is None else y
+        self.lib.ewo_spmv_csr_mt(C.c_int64(m.nrows), C.c_int64(m.ncols), _ip(m.row_offsets),
+                                 _ip(m.col_indices), _fp(m.values), _fp(x), _fp(y), C.c_int(int(threads)))
+        return y
+
     def extract_diagonal(self, m: Csr):
         d = np.empty(m.nrows, np.float64)
         self.lib.ewo_extract_diagonal(C.c_int64(m.nrows), C.c_int64(m.ncols), _ip(m.row_offsets),
