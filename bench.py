@@ -302,6 +302,15 @@ def dist_operator(args, rank, world):
 # ---------------------------------------------------------------------------
 # GPU arms
 # ---------------------------------------------------------------------------
+def k1_label(k, info):
+    """Which K1 kernel form layout_spmv launches for this layout (ew_spmv.cu)."""
+    if info.narrow_slots:
+        return "k1_kernel (16-bit columns on narrow warps, compact_layout)"
+    if info.stored_slots * 12 > 64 << 20 and info.stored_slots >= 24 * info.nrows:
+        return "k1_stream_kernel (grid-stride K1: layout beyond L2, >= 24 slots/row)"
+    return "k1_kernel"
+
+
 def run_spmv(args, rank, world, local):
     if world > 1:
         return run_spmv_dist(args, rank, world, local)
@@ -352,6 +361,12 @@ def run_spmv(args, rank, world, local):
     # r/rs apply); its per-launch time is the step time when launches == steps
     kern_ms = ms_local if launches == args.steps else None
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9 if kern_ms else None
+    # the bytes the layout actually streams: 16-bit columns on the narrow
+    # warps (compact_layout), int32 elsewhere, padding slots included
+    kinfo = k.info()
+    slots, narrow = int(kinfo.stored_slots), int(kinfo.narrow_slots)
+    streamed = 8 * slots + 2 * narrow + 4 * (slots - narrow) + 8 * n + 8 * nc
+    streamed_gbs = streamed / (kern_ms * 1e-3) / 1e9 if kern_ms else None
 
     # end-to-end through the C ABI with pinned host buffers
     xh = torch.empty(nc, dtype=torch.float64, pin_memory=True)
@@ -396,8 +411,13 @@ def run_spmv(args, rank, world, local):
                      "frac": round(achieved / hbm, 4) if achieved else None,
                      "traffic": ncu_traffic(f"{args.config}/{args.kernel}") if args.scale == 1.0 else None,
                      "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
-                     "kernel": ("k1_stream_kernel (grid-stride K1: layout beyond L2, >= 24 slots/row)" if args.config in ("c2", "c5full") else "k1_kernel") if args.kernel.startswith("k1") else "k2_kernel",
-                     "algorithmic_bytes_per_launch": alg_bytes},
+                     "kernel": k1_label(k, kinfo) if args.kernel.startswith("k1") else "k2_kernel",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "streamed_bytes_per_launch": streamed,
+                     "streamed_frac": round(streamed_gbs / hbm, 4) if streamed_gbs else None,
+                     "note": "achieved/frac: the reference format's bytes (12 B/nnz + 8 n + 8 ncols, SURVEY 8d) "
+                             "over the kernel time; streamed_frac: the bytes this layout moves (16-bit columns "
+                             "on %.1f%% of the slots) over the same time" % (100.0 * narrow / max(slots, 1))},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
                 "call_ms_min_median_max": [round(float(calls_ms.min()), 4), round(float(np.median(calls_ms)), 4),

@@ -111,6 +111,8 @@ typedef struct ew_layout_info {
     int64_t stored_slots; /* WarpLayoutK1/K2::stored_slots (warp_layout.cpp:20-29) */
     int64_t threshold;    /* K2 only */
     int64_t device_bytes; /* HBM held by the layout */
+    int64_t narrow_slots; /* K1: slots whose columns stream as 16-bit offsets
+                             from a per-warp base (0: all int32) */
 } ew_layout_info;
 
 /* Host views of a layout, in the reference's int64/double element types.
@@ -156,6 +158,7 @@ typedef struct ew_kernel_info {
     int32_t has_perm;     /* PreparedKernel::perm set (r/rs variants) */
     int32_t layout_kind;  /* 0 = csr_ref, else ew_layout_kind */
     int64_t device_bytes;
+    int64_t narrow_slots; /* as ew_layout_info::narrow_slots */
 } ew_kernel_info;
 
 /* ---- errors / library ---------------------------------------------------- */

@@ -337,6 +337,7 @@ ew_status ew_layout_get_info(ew_layout l, ew_layout_info* info) {
         info->stored_slots = d.stored_slots;
         info->threshold = d.threshold;
         info->device_bytes = static_cast<int64_t>(d.device_bytes());
+        info->narrow_slots = d.compact ? d.narrow_slots : 0;
     });
 }
 
@@ -448,6 +449,7 @@ ew_status ew_kernel_get_info(ew_kernel k, ew_kernel_info* info) {
         info->device_bytes = static_cast<int64_t>(
             d.layout ? d.layout->device_bytes()
                      : d.csr->device_bytes() + (d.format ? d.format->device_bytes() : size_t{0}));
+        info->narrow_slots = d.layout && d.layout->compact ? d.layout->narrow_slots : 0;
     });
 }
 

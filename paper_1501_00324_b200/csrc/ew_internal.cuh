@@ -168,12 +168,19 @@ struct LayoutData {
     DevBuf<int64_t> warp_offset;
     DevBuf<int32_t> maxrows, rows_in_warp, reduction, rows_offset_warp;
     DevBuf<int32_t> fwd, inv, slen;
+    // K1 with every warp's columns inside 0xFFFF of each other: the kernels
+    // stream 16-bit offsets from the warp's smallest column instead of the
+    // int32 columns (which stay for export / refresh maps)
+    int compact = 0;
+    int64_t narrow_slots = 0;  // slots outside the wide (int32) warps
+    DevBuf<uint16_t> cols16;   // per slot: col - col_base[w], 0xFFFF = padding (column 0)
+    DevBuf<int32_t> col_base;  // per warp
     DevBuf<int64_t> slot_map;  // lazily built value_slot_map (export)
     DevBuf<int64_t> src_map;   // lazily built per-slot source entry (values-only refresh)
     size_t device_bytes() const {
         return values.bytes() + cols.bytes() + warp_offset.bytes() + maxrows.bytes() +
                rows_in_warp.bytes() + reduction.bytes() + rows_offset_warp.bytes() + fwd.bytes() +
-               inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes();
+               inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes() + cols16.bytes() + col_base.bytes();
     }
 };
 

@@ -9,6 +9,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "ew_internal.cuh"
 
 namespace ew {
@@ -281,6 +283,58 @@ __global__ void iota_kernel(int64_t* __restrict__ out, int64_t n) {
 }
 
 
+// ---- compact (16-bit) columns for K1 ---------------------------------------
+// One hardware warp per layout warp (grid-stride): the smallest and largest
+// column over the warp's real entries (padding excluded).
+__global__ void compact_range_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                     const int32_t* __restrict__ maxrows, const int32_t* __restrict__ rows_in_warp,
+                                     const int32_t* __restrict__ slen, int32_t ws, int32_t ws_log2, int64_t nwarps,
+                                     int32_t* __restrict__ base, int64_t* fail) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = gw; w < nwarps; w += nhw) {
+        const int64_t n = int64_t(maxrows[w]) * ws, off = woff[w];
+        const int32_t nr = rows_in_warp[w];
+        int32_t mn = 0x7fffffff, mx = -1;
+        for (int64_t i = lane; i < n; i += 32) {
+            const int32_t l = static_cast<int32_t>(i & (ws - 1));
+            const int64_t j = i >> ws_log2;
+            if (l >= nr || j >= slen[w * ws + l]) continue;
+            const int32_t c = cols[off + i];
+            mn = min(mn, c);
+            mx = max(mx, c);
+        }
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) {
+            const bool wide = mx >= 0 && int64_t(mx) - mn >= 0xFFFF;
+            base[w] = wide ? -1 : (mx < 0 ? 0 : mn);
+            if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(fail), static_cast<unsigned long long>(n));
+        }
+    }
+}
+
+__global__ void compact_encode_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                      const int32_t* __restrict__ maxrows, const int32_t* __restrict__ rows_in_warp,
+                                      const int32_t* __restrict__ slen, int32_t ws, int32_t ws_log2, int64_t nwarps,
+                                      const int32_t* __restrict__ base, uint16_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = gw; w < nwarps; w += nhw) {
+        const int64_t n = int64_t(maxrows[w]) * ws, off = woff[w];
+        const int32_t nr = rows_in_warp[w], b = base[w];
+        if (b < 0) continue;  // stays on the int32 slab
+        for (int64_t i = lane; i < n; i += 32) {
+            const int32_t l = static_cast<int32_t>(i & (ws - 1));
+            const int64_t j = i >> ws_log2;
+            const bool valid = l < nr && j < slen[w * ws + l];
+            out[off + i] = valid ? static_cast<uint16_t>(cols[off + i] - b) : uint16_t{0xFFFF};
+        }
+    }
+}
+
 unsigned fill_grid(int64_t nwarps) {
     // 8 hardware warps per CTA, enough CTAs to cover every SM several times.
     int64_t g = (nwarps + 7) / 8;
@@ -432,6 +486,43 @@ std::shared_ptr<CsrData> reorder(const CsrData& m, const int64_t* fwd_in, bool r
     return out;
 }
 
+// 16-bit columns for the K1 warps whose real columns lie within 0xFFFF of
+// each other (mesh matrices in a natural or banded order: all but a few
+// warps of boundary rows); those warps stream 10 instead of 12 bytes per
+// slot, the rest keep the int32 slab (col_base < 0). Only for slabs that
+// stream from HBM (over 64 MB of values + columns: config 2's SpMV 163.6 ->
+// 158.0 us); on L2-resident ones the offset decode sits in the gather's
+// dependency chain and costs more than the bytes it saves (config 1: 5.9 ->
+// 6.3 us). Skipped when over a quarter of the slots are in wide warps.
+// EW_COMPACT=0: off; EW_COMPACT=2: at any size (tests).
+static void compact_layout(LayoutData& l, cudaStream_t s) {
+    static const int mode = [] {
+        const char* e = std::getenv("EW_COMPACT");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (mode == 0 || l.nslots == 0) return;
+    if (mode == 1 && l.nslots * 12 <= (64ll << 20)) return;
+    DevBuf<int32_t> base(l.nwarps);
+    Scratch<int64_t> fail(1, s);  // slots of warps whose columns span >= 0xFFFF
+    EW_CUDA_CHECK(cudaMemsetAsync(fail.get(), 0, sizeof(int64_t), s));
+    compact_range_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
+                                                             l.rows_in_warp.get(), l.slen.get(), l.ws, l.ws_log2,
+                                                             l.nwarps, base.get(), fail.get());
+    launched("compact_range_kernel");
+    int64_t wide = 0;
+    EW_CUDA_CHECK(cudaMemcpyAsync(&wide, fail.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (wide * 4 > l.nslots) return;  // mostly wide warps: not worth a second column slab
+    l.cols16.alloc(l.nslots);
+    compact_encode_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
+                                                              l.rows_in_warp.get(), l.slen.get(), l.ws, l.ws_log2,
+                                                              l.nwarps, base.get(), l.cols16.get());
+    launched("compact_encode_kernel");
+    l.col_base = std::move(base);
+    l.narrow_slots = l.nslots - wide;
+    l.compact = 1;
+}
+
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s) {
@@ -561,6 +652,7 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
                                                   l.cols.get());
         launched("fill_kernel");
     }
+    if (kind == EW_LAYOUT_K1 && !l.row_major && nw) compact_layout(l, s);
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     return L;
 }

@@ -65,23 +65,45 @@ struct K1Args {
     int32_t ws, ws_log2;
     const double* xg;  // SPLIT_X: columns >= nown read xg[c - nown] (a ghost tail)
     int32_t nown;
+    const uint16_t* cols16;   // COMPACT: 16-bit column offsets (LayoutData::cols16)
+    const int32_t* col_base;  // COMPACT: per-warp smallest column
 };
+
+__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p, uint64_t pol) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                 : "=h"(v)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+// Column sources of a lane sum: the int32 slab, or the compact one (16-bit
+// offsets from the warp's smallest column, 0xFFFF = padding = column 0).
+__device__ __forceinline__ auto cols32(const int32_t* __restrict__ cols) {
+    return [cols](int64_t i, uint64_t pol) { return ld_stream(cols + i, pol); };
+}
+__device__ __forceinline__ auto cols16(const uint16_t* __restrict__ c16, int32_t base) {
+    return [c16, base](int64_t i, uint64_t pol) {
+        const uint16_t d = ld_stream(c16 + i, pol);
+        return d == 0xFFFFu ? 0 : base + static_cast<int32_t>(d);
+    };
+}
 
 // Serial lane sum over j in [0, mx) at stride `step` from slot s, unrolled by
 // 8 so eight value/column loads and then eight x gathers are in flight per
 // thread before the (order-preserving) accumulation chain consumes them; the
 // last mx % 4 steps go in one predicated block (two round trips, not two per
 // step).
-template <typename XLoad>
-__device__ __forceinline__ double lane_sum_x(const double* __restrict__ vals, const int32_t* __restrict__ cols,
-                                             XLoad ld_x, int64_t s, int64_t step, int32_t mx, uint64_t pol) {
+template <typename ColLoad, typename XLoad>
+__device__ __forceinline__ double lane_sum_x(const double* __restrict__ vals, ColLoad ld_c, XLoad ld_x, int64_t s,
+                                             int64_t step, int32_t mx, uint64_t pol) {
     double sum = 0.0;
     int32_t j = 0;
     for (; j + 8 <= mx; j += 8) {
         int32_t c[8];
         double v[8], xv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] = ld_stream(cols + s + u * step, pol);
+        for (int u = 0; u < 8; ++u) c[u] = ld_c(s + u * step, pol);
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = ld_stream(vals + s + u * step, pol);
 #pragma unroll
@@ -94,7 +116,7 @@ __device__ __forceinline__ double lane_sum_x(const double* __restrict__ vals, co
         int32_t c[4];
         double v[4], xv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) c[u] = ld_stream(cols + s + u * step, pol);
+        for (int u = 0; u < 4; ++u) c[u] = ld_c(s + u * step, pol);
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = ld_stream(vals + s + u * step, pol);
 #pragma unroll
@@ -111,7 +133,7 @@ __device__ __forceinline__ double lane_sum_x(const double* __restrict__ vals, co
         double v[3], xv[3];
 #pragma unroll
         for (int u = 0; u < 3; ++u)
-            if (u < rem) c[u] = ld_stream(cols + s + u * step, pol);
+            if (u < rem) c[u] = ld_c(s + u * step, pol);
 #pragma unroll
         for (int u = 0; u < 3; ++u)
             if (u < rem) v[u] = ld_stream(vals + s + u * step, pol);
@@ -134,7 +156,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals, cons
     // where the hint cost 0.5% on config 2)
     uint64_t keep;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    return lane_sum_x(vals, cols, [x, keep](int32_t c) {
+    return lane_sum_x(vals, cols32(cols), [x, keep](int32_t c) {
         double v;
         asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(keep));
         return v;
@@ -144,7 +166,7 @@ __device__ __forceinline__ double lane_sum(const double* __restrict__ vals, cons
 __device__ __forceinline__ double lane_sum_ldg(const double* __restrict__ vals, const int32_t* __restrict__ cols,
                                                const double* __restrict__ x, int64_t s, int64_t step, int32_t mx,
                                                uint64_t pol) {
-    return lane_sum_x(vals, cols, [x](int32_t c) { return __ldg(x + c); }, s, step, mx, pol);
+    return lane_sum_x(vals, cols32(cols), [x](int32_t c) { return __ldg(x + c); }, s, step, mx, pol);
 }
 
 // x split in two arrays: owned columns [0, nown) in x, the ghost tail in xg
@@ -152,14 +174,42 @@ __device__ __forceinline__ double lane_sum_ldg(const double* __restrict__ vals, 
 __device__ __forceinline__ double lane_sum_split(const double* __restrict__ vals, const int32_t* __restrict__ cols,
                                                  const double* __restrict__ x, const double* __restrict__ xg,
                                                  int32_t nown, int64_t s, int64_t step, int32_t mx, uint64_t pol) {
-    return lane_sum_x(vals, cols, [x, xg, nown](int32_t c) { return c < nown ? __ldg(x + c) : __ldg(xg + (c - nown)); },
+    return lane_sum_x(vals, cols32(cols), [x, xg, nown](int32_t c) { return c < nown ? __ldg(x + c) : __ldg(xg + (c - nown)); },
                       s, step, mx, pol);
+}
+
+// One K1 lane sum of layout warp w. COMPACT: 16-bit columns (LayoutData::
+// cols16: 10 instead of 12 bytes per slot streamed) for the warps that have
+// them; x gathers with the evict_last hint either way.
+template <bool COMPACT>
+__device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, int64_t step, int32_t mx,
+                                         uint64_t pol) {
+    if (COMPACT) {
+        const int32_t base = a.col_base[w];  // < 0: this warp's columns span too far, int32 slab
+        if (base >= 0) {
+            const double* x = a.x;
+            uint64_t keep;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+            return lane_sum_x(a.values, cols16(a.cols16, base), [x, keep](int32_t c) {
+                double v;
+                asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(keep));
+                return v;
+            }, s, step, mx, pol);
+        }
+    }
+    return lane_sum(a.values, a.cols, a.x, s, step, mx, pol);
 }
 
 // K1 / K1r / K1rs (warp_spmv.cpp:9-60): one thread per sorted row position.
 // SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
-template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false>
-__global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
+#ifndef EW_K1C_MINB
+#define EW_K1C_MINB 5
+#endif
+#ifndef EW_K1P_MINB
+#define EW_K1P_MINB 8
+#endif
+template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool COMPACT = false>
+__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_kernel(K1Args a) {
     pdl_wait();
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= a.nrows || (a.done && *a.done)) return;
@@ -174,7 +224,7 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
         const int32_t mx = a.maxrows[w];
         const int64_t s = a.woff[w] + (ROW_MAJOR ? int64_t(lane) * mx : lane);
         sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, ROW_MAJOR ? 1 : a.ws, mx, pol)
-                      : lane_sum(a.values, a.cols, a.x, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
+                      : k1_row<COMPACT>(a, w, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
     }
     a.y[target] = sum;
     pdl_trigger();
@@ -191,7 +241,9 @@ __global__ void __launch_bounds__(256, 8) k1_kernel(K1Args a) {
 // 7.6 -> 9.1 us), and short-row gather-bound ones (config 4, 15 per row)
 // lose 1-5%, so layout_spmv picks by size and row length (the CG's fused
 // p.q kernel likewise: config-2-sized slab CG +4.8%). Same arithmetic,
-// bit-identical results.
+// bit-identical results. Layouts with 16-bit columns (compact_layout) run the
+// plain form instead: with the narrower column loads the stream form spills
+// more (221 us cold on config 2) and the plain one wins (158.0 us vs 163.6).
 template <bool SORTED, bool SCATTER, bool SPLIT_X = false>
 __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
     pdl_wait();
@@ -232,8 +284,8 @@ inline bool streams(const LayoutData& l) {
 // each row adds x[target] * y[target] to its CTA's fixed-order partial;
 // cg::dot_final_kernel sums the partials and decides. The CTA only stores
 // its partial: no fence or atomic holds it past its last row.
-template <bool SORTED, bool SCATTER>
-__global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
+template <bool SORTED, bool SCATTER, bool COMPACT = false>
+__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -245,7 +297,7 @@ __global__ void __launch_bounds__(256, 8) k1_dot_kernel(K1Args a, double* __rest
         if (active) {
             const int64_t w = p >> a.ws_log2;
             const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
-            sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+            sum = k1_row<COMPACT>(a, w, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
         }
         const int64_t t = SCATTER ? a.fwd[p] : p;
         a.y[t] = sum;
@@ -373,13 +425,16 @@ __global__ void k2_wide_kernel(K2Args a) {
 }
 
 template <bool SORTED, bool SCATTER>
-void launch_k1(const K1Args& a, bool row_major, bool stream_form, cudaStream_t s) {
-    if (stream_form && !row_major)
-        launch_pdl(k1_stream_kernel<SORTED, SCATTER>, grid_for(a.nrows), kBlock, s, a);
-    else if (row_major)
-        launch_pdl(k1_kernel<SORTED, SCATTER, true>, grid_for(a.nrows), kBlock, s, a);
+void launch_k1(const K1Args& a, bool row_major, bool stream_form, bool compact, cudaStream_t s) {
+    const unsigned g = grid_for(a.nrows);
+    if (row_major)
+        launch_pdl(k1_kernel<SORTED, SCATTER, true>, g, kBlock, s, a);
+    else if (compact)
+        launch_pdl(k1_kernel<SORTED, SCATTER, false, false, true>, g, kBlock, s, a);
+    else if (stream_form)
+        launch_pdl(k1_stream_kernel<SORTED, SCATTER>, g, kBlock, s, a);
     else
-        launch_pdl(k1_kernel<SORTED, SCATTER, false>, grid_for(a.nrows), kBlock, s, a);
+        launch_pdl(k1_kernel<SORTED, SCATTER, false, false, false>, g, kBlock, s, a);
     launched("k1_kernel");
 }
 
@@ -422,19 +477,26 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     }
     if (l.kind != EW_LAYOUT_K1) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
-             l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
+             l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
+             l.cols16.get(), l.col_base.get()};
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
     auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink.partials); };
-    if (streams(l)) {
+    const bool c = l.compact != 0;
+    if (c) {
+        if (l.sorted)
+            scatter ? go(k1_dot_kernel<true, true, true>) : go(k1_dot_kernel<true, false, true>);
+        else
+            scatter ? go(k1_dot_kernel<false, true, true>) : go(k1_dot_kernel<false, false, true>);
+    } else if (streams(l)) {
         if (l.sorted)
             scatter ? go(k1_dot_stream_kernel<true, true>) : go(k1_dot_stream_kernel<true, false>);
         else
             scatter ? go(k1_dot_stream_kernel<false, true>) : go(k1_dot_stream_kernel<false, false>);
     } else if (l.sorted) {
-        scatter ? go(k1_dot_kernel<true, true>) : go(k1_dot_kernel<true, false>);
+        scatter ? go(k1_dot_kernel<true, true, false>) : go(k1_dot_kernel<true, false, false>);
     } else {
-        scatter ? go(k1_dot_kernel<false, true>) : go(k1_dot_kernel<false, false>);
+        scatter ? go(k1_dot_kernel<false, true, false>) : go(k1_dot_kernel<false, false, false>);
     }
     launched("k1_dot_kernel");
     const unsigned nparts = grid * (256 / 32);  // one partial per SpMV warp
@@ -450,12 +512,13 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     if (l.nrows == 0) return;
     if (l.kind == EW_LAYOUT_K1) {
         K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
-                 l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0};
-        const bool rm = l.row_major != 0, sf = streams(l);
+                 l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
+             l.cols16.get(), l.col_base.get()};
+        const bool rm = l.row_major != 0, sf = streams(l), c = l.compact != 0;
         if (l.sorted) {
-            scatter ? launch_k1<true, true>(a, rm, sf, s) : launch_k1<true, false>(a, rm, sf, s);
+            scatter ? launch_k1<true, true>(a, rm, sf, c, s) : launch_k1<true, false>(a, rm, sf, c, s);
         } else {
-            scatter ? launch_k1<false, true>(a, rm, sf, s) : launch_k1<false, false>(a, rm, sf, s);
+            scatter ? launch_k1<false, true>(a, rm, sf, c, s) : launch_k1<false, false>(a, rm, sf, c, s);
         }
         return;
     }
@@ -478,7 +541,8 @@ void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, i
     require(l.kind == EW_LAYOUT_K1 && !l.row_major, "split-x SpMV: K1 column-major layouts only");
     if (l.nrows == 0) return;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
-             l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, xg, static_cast<int32_t>(nown)};
+             l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, xg, static_cast<int32_t>(nown),
+             nullptr, nullptr};
     if (streams(l)) {
         if (l.sorted)
             launch_pdl(k1_stream_kernel<true, true, true>, grid_for(a.nrows), kBlock, s, a);

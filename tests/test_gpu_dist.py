@@ -208,7 +208,10 @@ def _ipc_worker(rank, world, port, q):
         dist.barrier()
         del d, d2
         dist.barrier()
-        q.put((rank, ok_spmv, ok_cg, res.iterations, ref.iterations))
+        detail = {"spmv_bad_calls": [i for i, y in enumerate(ys) if not same_up_to_zero_sign(y, single[r0:r1])],
+                  "converged": res.converged, "it": res.iterations, "ref_it": ref.iterations,
+                  "hist_ok": hist_ok(res.residual_history, ref.residual_history)}
+        q.put((rank, ok_spmv, ok_cg, detail, ref.iterations))
         dist.destroy_process_group()
     except Exception as e:  # reported to the parent
         q.put((rank, False, False, repr(e), None))
@@ -233,7 +236,7 @@ def test_ipc_transport_two_processes(ew):
         p.join(timeout=60)
     for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
         assert ok_spmv, (rank, it)
-        assert ok_cg, (rank, it, ref_it)
+        assert ok_cg, (rank, it)
 
 
 def test_bench_two_ranks_functional(tmp_path):
