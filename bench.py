@@ -268,6 +268,15 @@ def build_slab(args, rank, world):
     return ng, ro, ci, v, bounds
 
 
+def step_times(ev0, marks):
+    """Per-step device times (ms) from the start event and one event per step."""
+    out, prev = [], ev0
+    for m in marks:
+        out.append(prev.elapsed_time(m))
+        prev = m
+    return out
+
+
 def dist_operator(args, rank, world):
     """This rank's partition of the slab operator. Transport "ipc" (default):
     CUDA IPC peer stores + mailboxes over NVLink, no NCCL on the data path;
@@ -542,10 +551,14 @@ def run_cg_dist(args, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record()
+        marks = []
         for _ in range(args.steps):
             res = d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record()
         ev1.record()
         torch.cuda.synchronize()
+    step_ms = [round(t, 3) for t in step_times(ev0, marks)]
     launches = capi.launch_count() - l0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
     it_s = iters / (ms * 1e-3)
@@ -569,7 +582,7 @@ def run_cg_dist(args, rank, world, local):
                                f"GPU ({nloc} rows/GPU, natural ordering)", "config": "c5-weak",
                    "iterations_per_step": iters, "nrows_total": int(n_all), "nnz_total": int(nnz_all),
                    "transport": getattr(args, "transport_used", args.transport),
-                   "final_residual": float(res.residual_history[-1])},
+                   "final_residual": float(res.residual_history[-1]), "step_ms_rank0": step_ms},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(per_gpu / hbm, 4), "traffic": None,
                      "algorithmic_bytes_per_iteration": b_it},
@@ -609,11 +622,15 @@ def run_cg(args, rank, world, local):
     with ClockSampler(local) as clk:
         ev0.record()
         tot = 0
+        marks = []
         for _ in range(args.steps):
             res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
             tot += res.iterations
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record()
         ev1.record()
         torch.cuda.synchronize()
+    step_ms = [round(t, 3) for t in step_times(ev0, marks)]
     launches = capi.launch_count() - l0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
     it_s = world * iters / (ms * 1e-3)
@@ -624,7 +641,7 @@ def run_cg(args, rank, world, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
                    "row_order": args.row_order, "iterations_per_step": iters, "nrows": n, "nnz": nnz,
-                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3)},
+                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3), "step_ms_rank0": step_ms},
         "roofline": None,
         "iteration_roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
                                "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
@@ -910,7 +927,7 @@ def main():
     p.add_argument("--iterations", type=int, default=1000)
     p.add_argument("--cpu-cg-iters", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cg-steps", type=int, default=2,
+    p.add_argument("--cg-steps", type=int, default=5,
                    help="spmv workload: also time this many 1000-iteration partitioned CG steps (0: skip)")
     args = p.parse_args()
     args.warmup = max(3, args.warmup)

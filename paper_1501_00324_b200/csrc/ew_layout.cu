@@ -512,7 +512,11 @@ static void compact_layout(LayoutData& l, cudaStream_t s) {
     int64_t wide = 0;
     EW_CUDA_CHECK(cudaMemcpyAsync(&wide, fail.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
-    if (wide * 4 > l.nslots) return;  // mostly wide warps: not worth a second column slab
+    static const double min_narrow = [] {
+        const char* e = std::getenv("EW_COMPACT_MIN");  // A/B runs: least narrow share
+        return e ? std::atof(e) : 0.75;
+    }();
+    if (double(l.nslots - wide) < min_narrow * double(l.nslots)) return;  // mostly wide warps
     l.cols16.alloc(l.nslots);
     compact_encode_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
                                                               l.rows_in_warp.get(), l.slen.get(), l.ws, l.ws_log2,
