@@ -100,7 +100,9 @@ class ClockSampler:
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
             t = time.time()
-            while not self.rows and time.time() - t < 5.0:  # sampler live before timing starts
+            # sampler live (and past its first queries, which can stall the
+            # GPU for tens of ms) before timing starts
+            while len(self.rows) < 6 and time.time() - t < 5.0:
                 time.sleep(0.01)
             self.rows.clear()
         except FileNotFoundError:
