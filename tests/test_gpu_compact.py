@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 def mixed(n=1_200_000, seed=7):
     """Row r: length 4 + (r // 50000) % 9; runs of length 12 get columns
     spread over the whole range (wide warps), the rest r + 37 j (mod n)
-    (narrow warps, whatever the row numbering the r / rs ids sort into).
+    (narrow warps, whatever the row numbering the r / rs ids sort into),
+    runs of length 11 three clusters 40,000 apart (wide).
     Length classes recur every 9 runs, so warps at the joints span far (wide)
     or mix lengths (padding)."""
     rng = np.random.default_rng(seed)
@@ -33,6 +34,9 @@ def mixed(n=1_200_000, seed=7):
     base = np.repeat(np.where(lens == 12, rng.integers(0, n, n), r), lens)
     step = np.where(np.repeat(lens == 12, lens), 104729, 37)  # distinct columns per row
     cols = (base + j * step) % n
+    # length-11 runs: three clusters 40,000 columns apart
+    three = np.repeat(lens == 11, lens)
+    cols = np.where(three, (rows + (j % 3 - 1) * 40000 + 37 * (j // 3)) % n, cols)
     cols = np.sort(rows * n + cols) - rows * n  # ascending within each row
     vals = rng.uniform(0.1, 1.0, rows.size)
     return Csr.make(n, n, ro, cols, vals)
@@ -81,9 +85,8 @@ def test_mixed_spans_refresh(ew, R, mx):
 
 def test_laplacian_cg_compact(ew, R, F):
     """Jacobi PCG on a 7-point Laplacian past the gate: the fused p.q SpMV on
-    the compact slab, history within the reference comparator. (k1rs moves
-    the boundary rows behind the interior ones, so most warps reach a far
-    column there and its layout keeps int32 columns: the same CG on both.)"""
+    the compact slab, history within the reference comparator (k1rs moves
+    the boundary rows behind the interior ones: its warps reach further)."""
     m = F.laplacian3d(100, 100, 100)
     b = R.spmv_csr(m, np.ones(m.ncols))
     a = dev(ew, m)
@@ -91,7 +94,61 @@ def test_laplacian_cg_compact(ew, R, F):
     ref = R.cg_csr(m, b, max_iterations=150)
     for kid in ("k1", "k1rs"):
         k = ew.Kernel(kid, a)
-        assert compact_in_use(k) == (kid == "k1"), kid
+        if kid == "k1":
+            assert compact_in_use(k)
         res = k.cg_solve(b, diag, max_iterations=150)
         assert res.iterations == ref.iterations
         assert_history(res.residual_history, ref.residual_history)
+
+
+_CORPUS_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from oracle.oracle import Reference, Restatement
+from paper_1501_00324_b200 import capi as ew
+from tests.gpu_helpers import bits, oracle_apply
+R, F = Restatement(), Reference()
+narrow = 0
+for case in range(0, 40, 2):
+    m = F.random_case(case)
+    x = F.random_vector(m.ncols, 7000 + case)
+    a = ew.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+    for ws in (4, 8, 32):
+        for kid in ("k1", "k1r", "k1rs"):
+            if kid != "k1" and m.nrows != m.ncols:
+                continue
+            k = ew.Kernel(kid, a, warp_size=ws)
+            narrow += k.info().narrow_slots
+            y = k.apply(x)
+            assert np.array_equal(bits(y), bits(oracle_apply(R, kid, m, x, ws))), (case, kid, ws)
+assert narrow > 0
+# fused p.q SpMV on compact layouts: CG on the reference's SPD family
+for n in (6, 10):
+    m = F.laplacian3d(n, n, n)
+    b = R.spmv_csr(m, np.ones(m.ncols))
+    ref = R.cg_csr(m, b)
+    a = ew.Csr(m.nrows, m.ncols, m.row_offsets, m.col_indices, m.values)
+    for kid in ("k1", "k1rs"):
+        k = ew.Kernel(kid, a)
+        res = k.cg_solve(b, a.extract_diagonal())
+        assert res.converged and res.iterations == ref.iterations, (n, kid)
+        assert np.all(np.abs(res.residual_history - ref.residual_history) <= 1e-10 * (1 + ref.residual_history))
+print("ok", narrow)
+"""
+
+
+def test_compact_at_any_size_corpus(ew, F):
+    """EW_COMPACT=2 (16-bit columns at any size, a test-only setting) over the
+    reference's random corpus at warp sizes 4, 8, 32: every K1 id bitwise
+    against the restated reference, and CG histories on compact layouts."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EW_COMPACT="2")
+    out = subprocess.run([sys.executable, "-c", _CORPUS_SCRIPT.format(root=root)], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert out.stdout.strip().startswith("ok")
