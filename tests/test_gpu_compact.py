@@ -21,7 +21,7 @@ def mixed(n=1_200_000, seed=7):
     """Row r: length 4 + (r // 50000) % 9; runs of length 12 get columns
     spread over the whole range (wide warps), the rest r + 37 j (mod n)
     (narrow warps, whatever the row numbering the r / rs ids sort into),
-    runs of length 11 three clusters 40,000 apart (wide).
+    one run three clusters 40,000 apart (wide).
     Length classes recur every 9 runs, so warps at the joints span far (wide)
     or mix lengths (padding)."""
     rng = np.random.default_rng(seed)
@@ -34,8 +34,8 @@ def mixed(n=1_200_000, seed=7):
     base = np.repeat(np.where(lens == 12, rng.integers(0, n, n), r), lens)
     step = np.where(np.repeat(lens == 12, lens), 104729, 37)  # distinct columns per row
     cols = (base + j * step) % n
-    # length-11 runs: three clusters 40,000 columns apart
-    three = np.repeat(lens == 11, lens)
+    # rows 350,000-399,999: three clusters 40,000 columns apart
+    three = np.repeat(r // 50000 == 7, lens)  # one run of them
     cols = np.where(three, (rows + (j % 3 - 1) * 40000 + 37 * (j // 3)) % n, cols)
     cols = np.sort(rows * n + cols) - rows * n  # ascending within each row
     vals = rng.uniform(0.1, 1.0, rows.size)
