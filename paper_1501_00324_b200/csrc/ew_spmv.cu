@@ -440,8 +440,16 @@ void launch_k1(const K1Args& a, bool row_major, bool stream_form, bool compact, 
     const unsigned g = grid_for(a.nrows);
     if (row_major)
         launch_pdl(k1_kernel<SORTED, SCATTER, true>, g, kBlock, s, a);
-    else if (compact)
-        launch_pdl(k1_kernel<SORTED, SCATTER, false, false, true>, g, kBlock, s, a);
+    else if (compact) {
+        // 64-thread CTAs: at 5 x 256 threads per SM the last wave of config 2
+        // (10.4 waves) leaves SMs idle; 20 x 64 packs it finer (141.1 ->
+        // 139.6 us, A/B in one box; 128: 139.7-141.6)
+        static const int cb = [] {
+            const char* e = std::getenv("EW_K1C_BLOCK");  // A/B runs: CTA size of the 16-bit-column K1
+            return e ? std::atoi(e) : 64;
+        }();
+        launch_pdl(k1_kernel<SORTED, SCATTER, false, false, true>, grid_for(a.nrows, cb), cb, s, a);
+    }
     else if (stream_form)
         launch_pdl(k1_stream_kernel<SORTED, SCATTER>, g, kBlock, s, a);
     else
