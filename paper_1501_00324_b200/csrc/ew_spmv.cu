@@ -500,8 +500,16 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
              l.cols16.get(), l.col_base.get()};
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
-    auto go = [&](auto kernel) { launch_pdl(kernel, grid, 256, s, a, sink.partials); };
     const bool c = l.compact != 0;
+    // the 16-bit-column form in 64-thread CTAs (as layout_spmv's); the
+    // partials stay one per warp, in warp order, and no more of them
+    static const int cb = [] {
+        const char* e = std::getenv("EW_K1C_DOT_BLOCK");  // A/B runs
+        return e ? std::atoi(e) : 64;
+    }();
+    const int block = c ? cb : 256;
+    const unsigned g = grid_for(l.nrows, block);
+    auto go = [&](auto kernel) { launch_pdl(kernel, g, block, s, a, sink.partials); };
     if (c) {
         if (l.sorted)
             scatter ? go(k1_dot_kernel<true, true, true>) : go(k1_dot_kernel<true, false, true>);
@@ -518,7 +526,7 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
         scatter ? go(k1_dot_kernel<false, true, false>) : go(k1_dot_kernel<false, false, false>);
     }
     launched("k1_dot_kernel");
-    const unsigned nparts = grid * (256 / 32);  // one partial per SpMV warp
+    const unsigned nparts = g * (block / 32);  // one partial per SpMV warp
     launch_pdl(cg::dot_final_kernel, static_cast<unsigned>(cg::dot_final_blocks(nparts)), cg::kRedBlock, s,
                (const double*)sink.partials, nparts, sink.partials + nparts, sink.tickets, sink.st, sink.dist,
                sink.slot);
