@@ -93,6 +93,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("EW_BENCH_NO_CLOCKS") == "1":  # diagnosis only: no sampler
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -929,7 +931,7 @@ def main():
     p.add_argument("--iterations", type=int, default=1000)
     p.add_argument("--cpu-cg-iters", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cg-steps", type=int, default=5,
+    p.add_argument("--cg-steps", type=int, default=10,
                    help="spmv workload: also time this many 1000-iteration partitioned CG steps (0: skip)")
     args = p.parse_args()
     args.warmup = max(3, args.warmup)
@@ -940,7 +942,7 @@ def main():
     if args.workload == "cg":
         args.permuted = args.permuted or args.kernel.endswith(("r", "rs"))
     if args.steps is None:
-        args.steps = 3 if args.workload == "cg" else 2000
+        args.steps = 10 if args.workload == "cg" else 2000
     if args.row_order is None:
         # CG on an r / rs kernel: the locality row order (same row sums,
         # EW_ROW_ORDER_LOCALITY); everything else the reference's order
