@@ -627,8 +627,11 @@ def run_cg(args, rank, world, local):
         ev0.record()
         tot = 0
         marks = []
+        host = []
         for _ in range(args.steps):
+            th = time.perf_counter()
             res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+            host.append(round((time.perf_counter() - th) * 1e3, 1))
             tot += res.iterations
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
@@ -645,7 +648,7 @@ def run_cg(args, rank, world, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
                    "row_order": args.row_order, "iterations_per_step": iters, "nrows": n, "nnz": nnz,
-                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3), "step_ms_rank0": step_ms},
+                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3), "step_ms_rank0": step_ms, "step_host_ms_rank0": host},
         "roofline": None,
         "iteration_roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
                                "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
