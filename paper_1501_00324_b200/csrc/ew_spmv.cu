@@ -202,9 +202,6 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
 
 // K1 / K1r / K1rs (warp_spmv.cpp:9-60): one thread per sorted row position.
 // SCATTER stores y[Pinv[p]] (K1); otherwise y[p] in sorted numbering.
-#ifndef EW_DOT_EARLY
-#define EW_DOT_EARLY 1
-#endif
 #ifndef EW_K1C_MINB
 #define EW_K1C_MINB 5
 #endif
@@ -296,21 +293,15 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_d
     if (p < a.nrows) {
         const uint64_t pol = evict_first_policy();
         double sum = 0.0;
-#if EW_DOT_EARLY
         // target and p[target] loaded with the metadata, not after the row sum
         const int64_t t = SCATTER ? a.fwd[p] : p;
         const double xt = a.x[t];
-#endif
         const bool active = SORTED ? p < a.n_active : a.slen[p] > 0;
         if (active) {
             const int64_t w = p >> a.ws_log2;
             const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
             sum = k1_row<COMPACT>(a, w, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
         }
-#if !EW_DOT_EARLY
-        const int64_t t = SCATTER ? a.fwd[p] : p;
-        const double xt = a.x[t];
-#endif
         a.y[t] = sum;
         v[0] = __dmul_rn(xt, sum);
     }
