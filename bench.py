@@ -386,7 +386,7 @@ def run_spmv(args, rank, world, local):
     xh.copy_(x.cpu())
     yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xn, yn = xh.numpy(), yh.numpy()
-    k_e2e = max(3, min(args.steps, 50))
+    k_e2e = max(3, min(args.steps, 200))
     for _ in range(2):
         apply(xn, yn)
     barrier(world)
