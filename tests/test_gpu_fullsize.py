@@ -36,9 +36,9 @@ def dev(ew, m):
 
 
 def test_config2_k1_bitwise(ew, R, c2):
-    """The default bench's kernel (the grid-stride stream form at this size)
-    against the restated reference K1, bit for bit; linearity and the
-    layout's padding count as size-independent checks."""
+    """The default bench's kernel (16-bit columns at this size) against the
+    restated reference K1, bit for bit, through host and device buffers;
+    linearity and the layout's padding count as size-independent checks."""
     a = dev(ew, c2)
     x = np.random.default_rng(1).uniform(0.1, 1.0, c2.ncols)
     k = ew.Kernel("k1", a)
@@ -51,6 +51,13 @@ def test_config2_k1_bitwise(ew, R, c2):
         R.free(lay)
     assert np.array_equal(bits(y), bits(want))
     assert rel_close(y, R.spmv_csr(c2, x), 1e-12)
+    # host buffers run the row-block pipeline; device buffers the whole
+    # layout, with 16-bit columns on every warp of this matrix
+    import torch
+
+    assert k.info().narrow_slots >= 0.99 * k.stored_slots
+    yd = k.apply(torch.tensor(x, device="cuda")).cpu().numpy()
+    assert np.array_equal(bits(yd), bits(want))
     x2 = np.random.default_rng(2).uniform(-1.0, 1.0, c2.ncols)
     lhs = k.apply(2.0 * x + x2)
     rhs = 2.0 * y + k.apply(x2)
