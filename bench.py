@@ -547,8 +547,12 @@ def run_cg_dist(args, rank, world, local):
     diag[rows[hit]] = v[hit]
     dd = torch.tensor(diag, device="cuda")
     iters = args.iterations
-    for _ in range(args.warmup):  # full-length steps: clocks ramp up from idle
-        d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
+    # full-length warm-up steps (clocks ramp up from idle), each result held
+    # while the next solve allocates its own, as in the timed loop (else the
+    # allocator's second solution buffer is first allocated inside it)
+    res = None
+    for _ in range(args.warmup):
+        res = d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
     torch.cuda.synchronize()
     barrier(world)
     l0 = capi.launch_count()
@@ -620,8 +624,12 @@ def run_cg(args, rank, world, local):
     bd = torch.tensor(b, device="cuda")
     dd = torch.tensor(diag, device="cuda")
     iters = args.iterations
-    for _ in range(args.warmup):  # full-length steps: clocks ramp up from idle
-        k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+    # full-length warm-up steps (clocks ramp up from idle), each result held
+    # while the next solve allocates its own, as in the timed loop (else the
+    # allocator's second solution buffer is first allocated inside it)
+    res = None
+    for _ in range(args.warmup):
+        res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
     torch.cuda.synchronize()
     barrier(world)
     l0 = capi.launch_count()
