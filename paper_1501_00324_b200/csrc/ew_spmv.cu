@@ -21,10 +21,6 @@ namespace ew {
 
 namespace {
 
-struct StreamPolicy {
-    uint64_t p;
-};
-
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
