@@ -40,10 +40,13 @@ CONFIGS = {
                gen="elasticity_box", dims=(86, 86, 86)),
     "c4": dict(name="Jacobi PCG 1000 it, jittered+renumbered tet ventricle-like mesh 171^3 nodes (5,000,211 rows)",
                gen="ventricle_box", dims=(170, 170, 170)),
-    # config 5 whole on one B200 (the partitioned runs use config-2-sized slabs per GPU)
+    # config 5 whole on one GPU through a plain prepared kernel (SpMV / CG)
     "c5full": dict(name="fp64 3-DOF linear-elasticity tet mesh 322^3 nodes (100,158,744 rows), one GPU",
                    gen="elasticity_box_slabbed", dims=(321, 321, 321)),
 }
+# config 5 for the partitioned CG: the same 100,158,744-row mesh at every N,
+# rank r generating only its z-slab of node layers (strong scaling)
+C5_DIMS = (321, 321, 321)
 
 
 def log(*a):
@@ -272,6 +275,25 @@ def build_slab(args, rank, world):
     return ng, ro, ci, v, bounds
 
 
+def build_c5_block(args, rank, world):
+    """Rank `rank`'s rows of config 5 (box(321, 321, 321), 3-DOF elasticity,
+    100,158,744 rows): node layers slab_layers(321, world)[rank:rank + 2],
+    generated slab by slab on host threads (strong scaling: the global mesh
+    is the same at every N)."""
+    from paper_1501_00324_b200 import workloads as W
+
+    nx, ny, nz = (max(2, int(round(d * args.scale))) for d in C5_DIMS)
+    layers = W.slab_layers(nz, world)
+    t = time.time()
+    workers = max(1, min(16, (os.cpu_count() or 8) // world))
+    rb, ng, ro, ci, v = W.box_rows_slabbed("elasticity", nx, ny, nz, layers[rank], layers[rank + 1],
+                                           workers=workers)
+    bounds = np.array([3 * (nx + 1) * (ny + 1) * k for k in layers], np.int64)
+    log(f"[bench] rank {rank}: config-5 layers [{layers[rank]}, {layers[rank + 1]}) of box({nx},{ny},{nz}): "
+        f"{ro.size - 1} rows, {ro[-1]} nnz, {time.time() - t:.1f}s ({workers} threads)")
+    return ng, ro, ci, v, bounds
+
+
 def step_times(ev0, marks):
     """Per-step device times (ms) from the start event and one event per step."""
     out, prev = [], ev0
@@ -281,15 +303,16 @@ def step_times(ev0, marks):
     return out
 
 
-def dist_operator(args, rank, world):
-    """This rank's partition of the slab operator. Transport "ipc" (default):
+def dist_operator(args, rank, world, shape="c2-slab"):
+    """This rank's partition of the slab operator ("c2-slab": a config-2-sized
+    block per GPU; "c5": its share of config 5). Transport "ipc" (default):
     CUDA IPC peer stores + mailboxes over NVLink, no NCCL on the data path;
     "nccl": ncclSend/Recv halos and ncclAllGather dots."""
     import torch.distributed as dist
 
     from paper_1501_00324_b200 import capi
 
-    ng, ro, ci, v, bounds = build_slab(args, rank, world)
+    ng, ro, ci, v, bounds = build_c5_block(args, rank, world) if shape == "c5" else build_slab(args, rank, world)
     kid = args.kernel if args.kernel in ("k1", "k2", "csr_ref") else "k1"
     t = time.time()
     transport = args.transport
@@ -309,6 +332,7 @@ def dist_operator(args, rank, world):
     info = d.info()
     log(f"[bench] rank {rank}: partitioned operator ({transport}) in {time.time() - t:.2f}s, {info['nghost']} ghosts, "
         f"{info['nsend']} sent per exchange")
+    info["bounds"] = bounds
     return d, ng, ro, ci, v, info
 
 
@@ -354,15 +378,23 @@ def run_spmv(args, rank, world, local):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    l0 = capi.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        # the timed loop is a few ms (shorter than one nvidia-smi sample):
+        # the sampler records the clocks over a >= 1 s soak of the same
+        # launches right before it, on the same stream, without a gap
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 1.0:
+            for _ in range(50):
+                apply(x, y, stream=stream)
+            torch.cuda.current_stream().synchronize()
+        l0 = capi.launch_count()
         ev0.record(stream)
         for _ in range(args.steps):
             apply(x, y, stream=stream)
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = capi.launch_count() - l0
+        launches = capi.launch_count() - l0
     barrier(world)
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local, world)
@@ -386,8 +418,8 @@ def run_spmv(args, rank, world, local):
     xh.copy_(x.cpu())
     yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xn, yn = xh.numpy(), yh.numpy()
-    k_e2e = max(3, min(args.steps, 200))
-    for _ in range(2):
+    k_e2e = 200
+    for _ in range(10):
         apply(xn, yn)
     barrier(world)
     calls = []
@@ -437,7 +469,8 @@ def run_spmv(args, rank, world, local):
                                            round(float(calls_ms.max()), 4)],
                 "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y"},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), window="1 s soak of the same launches right before the timed loop + the "
+                                              "timed loop"),
         "prepare_s": round(t_prepare, 3),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -527,24 +560,48 @@ def run_spmv_dist(args, rank, world, local):
     }
 
 
-def run_cg_dist(args, rank, world, local):
-    """Row-partitioned Jacobi PCG, 1000 iterations, weak scaling."""
+def reference_cg_sample(ro, ci, v, rows, iters):
+    """The reference's cg_solve(csr_ref) on the principal submatrix of the
+    leading `rows` rows (SPD like the whole operator), b = A 1, 1 thread.
+    Returns (it/s, nnz of the sample, seconds)."""
+    from oracle.oracle import Csr, Reference
+
+    F = Reference()
+    end = int(ro[rows])
+    keep = ci[:end] < rows
+    row_of = np.repeat(np.arange(rows), np.diff(ro[:rows + 1]))
+    sro = np.zeros(rows + 1, np.int64)
+    np.cumsum(np.bincount(row_of[keep], minlength=rows), out=sro[1:])
+    m = Csr.make(rows, rows, sro, ci[:end][keep], v[:end][keep])
+    b = F.spmv_csr(m, np.ones(rows))
+    t = time.perf_counter()
+    res = F.cg("csr_ref", m, b, tol=1e-300, max_iterations=iters)
+    dt = time.perf_counter() - t
+    return res.iterations / dt, m.nnz, dt
+
+
+def run_cg_dist(args, rank, world, local, shape="c2-slab"):
+    """Row-partitioned Jacobi PCG, 1000 iterations per step. shape "c5":
+    config 5 (100M rows) split over the ranks (strong scaling); "c2-slab":
+    a config-2-sized slab per rank (weak scaling)."""
     import torch
-    import torch.distributed as dist
 
     from paper_1501_00324_b200 import capi
 
     hbm, peak_src = peaks()
-    d, ng, ro, ci, v, info = dist_operator(args, rank, world)
+    d, ng, ro, ci, v, info = dist_operator(args, rank, world, shape)
     nloc, nnz = ro.size - 1, int(ro[-1])
     ones = torch.ones(d.owned, dtype=torch.float64, device="cuda")
     b = d.spmv(ones)  # b = A * 1 (ellwarp_cli.cpp:192-195)
     # diagonal of the owned rows (global column == global row)
-    rows = np.repeat(np.arange(nloc), np.diff(ro))
-    glob_row = rows + int(info["row_begin"])
     diag = np.zeros(nloc)
-    hit = ci == glob_row
-    diag[rows[hit]] = v[hit]
+    r0 = int(info["row_begin"])
+    for a in range(0, nloc, 1 << 22):  # in row chunks: config 5 at N=1 has 4.5G entries
+        e = min(nloc, a + (1 << 22))
+        lo, hi = int(ro[a]), int(ro[e])
+        rows = np.repeat(np.arange(a, e), np.diff(ro[a:e + 1]))
+        hit = ci[lo:hi] == rows + r0
+        diag[rows[hit]] = v[lo:hi][hit]
     dd = torch.tensor(diag, device="cuda")
     iters = args.iterations
     # full-length warm-up steps (clocks ramp up from idle), each result held
@@ -557,19 +614,22 @@ def run_cg_dist(args, rank, world, local):
     barrier(world)
     l0 = capi.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ran = []
     with ClockSampler(local) as clk:
         ev0.record()
         marks = []
         for _ in range(args.steps):
             res = d.cg_solve(b, dd, tol=1e-300, max_iterations=iters)
+            ran.append(res.iterations)
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
         ev1.record()
         torch.cuda.synchronize()
+    assert all(r == iters for r in ran), f"a timed solve stopped early: {ran}"
     step_ms = [round(t, 3) for t in step_times(ev0, marks)]
     launches = capi.launch_count() - l0
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
-    it_s = iters / (ms * 1e-3)
+    it_s = sum(ran) / args.steps / (ms * 1e-3)
     nnz_all, n_all = sum_over_ranks([float(nnz), float(nloc)], world)
     b_it = 12 * nnz_all + 104 * n_all + (12 * nnz_all + 24 * n_all) / 50
     per_gpu = b_it / world * it_s / 1e9
@@ -579,94 +639,93 @@ def run_cg_dist(args, rank, world, local):
     t = time.perf_counter()
     d.cg_solve(bh, dh, tol=1e-300, max_iterations=iters)
     e2e_s = max_over_ranks(time.perf_counter() - t, world)
-    return {
+    strong = shape == "c5"
+    if strong:
+        workload = (f"row-partitioned Jacobi PCG {iters} it, config 5: 3-DOF elasticity box(321,321,321) "
+                    f"= {int(n_all):,} rows, {int(nnz_all):,} nnz over {world} GPU(s), z-slab row blocks "
+                    f"(rank 0: {nloc} rows)")
+    else:
+        workload = (f"row-partitioned Jacobi PCG {iters} it, elasticity box slab of 87 node layers per "
+                    f"GPU ({nloc} rows/GPU, natural ordering)")
+    out = {
         "e2e": {"value": round(iters / e2e_s, 2), "unit": "it/s", "h2d_bytes_per_step": 16 * nloc,
                 "d2h_bytes_per_step": 8 * nloc + 8 * (iters + 1),
-                "path": "ew_dist_cg_solve(EW_MEM_HOST) per rank"},
+                "path": "ew_dist_cg_solve(EW_MEM_HOST) per rank: b, diag in, solution + history out"},
         "metric": "CG iterations/s", "value": round(it_s, 2), "unit": "it/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"row-partitioned Jacobi PCG {iters} it, elasticity box slab of 87 node layers per "
-                               f"GPU ({nloc} rows/GPU, natural ordering)", "config": "c5-weak",
-                   "iterations_per_step": iters, "nrows_total": int(n_all), "nnz_total": int(nnz_all),
-                   "transport": getattr(args, "transport_used", args.transport),
-                   "final_residual": float(res.residual_history[-1]), "step_ms_rank0": step_ms},
+        "config": {"workload": workload, "config": "c5" if strong else "c5-weak",
+                   "iterations_per_step": iters, "iterations_run": ran, "nrows_total": int(n_all),
+                   "nnz_total": int(nnz_all), "transport": getattr(args, "transport_used", args.transport),
+                   "ghosts_rank0": info["nghost"], "final_residual": float(res.residual_history[-1]),
+                   "step_ms_rank0": step_ms},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(per_gpu / hbm, 4),
-                     "traffic": ncu_traffic("c5/cg_k1_dot") if args.scale == 1.0 else None,
-                     "traffic_source": "profiles/ncu_traffic.json[c5/cg_k1_dot]: DRAM bytes per launch of the "
-                                       "iteration's dominant kernel, the fused SpMV + p.q (one per iteration)",
-                     "algorithmic_bytes_per_iteration": b_it},
+                     "traffic": ncu_traffic("c5/cg_k1_dot") if args.scale == 1.0 and not strong else None,
+                     "traffic_source": "profiles/ncu_traffic.json: DRAM bytes per launch of the iteration's dominant "
+                                       "kernel, the fused SpMV + p.q (one per iteration)",
+                     "algorithmic_bytes_per_iteration": b_it,
+                     "note": "per-GPU share of 12 nnz + 104 n + refresh bytes per iteration / max-over-ranks "
+                             "iteration time"},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    if strong and rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = 3 * 322 * 322 * 8  # the first 8 node layers
+        rate, snnz, dt = reference_cg_sample(ro, ci, v, rows, max(2, args.cpu_cg_iters))
+        out["cpu_baseline"] = {"value": round(rate * snnz / nnz_all, 5), "unit": "it/s", "cores": 1,
+                               "kind": "reference",
+                               "sample": f"cg_solve(csr_ref) for {max(2, args.cpu_cg_iters)} iterations on the "
+                                         f"principal submatrix of config 5's first 8 node layers ({rows} rows, "
+                                         f"{snnz} nnz, {rate:.3f} it/s, {dt:.1f}s; oracle/_ref, 1 thread), "
+                                         "scaled by nnz to the whole matrix"}
+    return out
 
 
-def run_cg(args, rank, world, local):
-    if world > 1 or args.config == "c5":
-        return run_cg_dist(args, rank, world, local)
+def cg_one_gpu(args, a, n, nc, nnz, bd, dd, b, diag, kernel, row_order, local):
+    """Time `args.steps` forced-length PCG solves of one prepared kernel on
+    one GPU (after `args.warmup` untimed ones). Returns the line's fields."""
     import torch
 
     from paper_1501_00324_b200 import capi
 
     hbm, peak_src = peaks()
-    n, nc, ro, ci, v = build_matrix(args.config, args.scale)
-    nnz = int(ro[-1])
-    a = capi.Csr(n, nc, ro, ci, v)
+    permuted = kernel.endswith(("r", "rs"))
     t = time.time()
-    k = capi.Kernel(args.kernel, a, threshold=args.threshold, row_order=args.row_order)
+    k = capi.Kernel(kernel, a, threshold=args.threshold, row_order=row_order)
     torch.cuda.synchronize()
     t_prepare = time.time() - t
-    log(f"[bench] prepare({args.kernel}, row_order={args.row_order}) {t_prepare:.2f}s")
-    diag = a.extract_diagonal()
-    b = a.spmv(np.ones(nc))  # b = A * 1 (ellwarp_cli.cpp:192-195)
-    del a  # the prepared kernel keeps only its layout
-    torch.cuda.empty_cache()
-    bd = torch.tensor(b, device="cuda")
-    dd = torch.tensor(diag, device="cuda")
+    log(f"[bench] prepare({kernel}, row_order={row_order}) {t_prepare:.2f}s")
     iters = args.iterations
-    # full-length warm-up steps (clocks ramp up from idle), each result held
-    # while the next solve allocates its own, as in the timed loop (else the
-    # allocator's second solution buffer is first allocated inside it)
     res = None
     for _ in range(args.warmup):
-        res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+        res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=permuted)
     torch.cuda.synchronize()
-    barrier(world)
     l0 = capi.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ran, marks, host = [], [], []
     with ClockSampler(local) as clk:
         ev0.record()
-        tot = 0
-        marks = []
-        host = []
         for _ in range(args.steps):
             th = time.perf_counter()
-            res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=args.permuted)
+            res = k.cg_solve(bd, dd, tol=1e-300, max_iterations=iters, permuted=permuted)
             host.append(round((time.perf_counter() - th) * 1e3, 1))
-            tot += res.iterations
+            ran.append(res.iterations)
             marks.append(torch.cuda.Event(enable_timing=True))
             marks[-1].record()
         ev1.record()
         torch.cuda.synchronize()
+    assert all(r == iters for r in ran), f"a timed solve stopped early: {ran}"
     step_ms = [round(t, 3) for t in step_times(ev0, marks)]
     launches = capi.launch_count() - l0
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
-    it_s = world * iters / (ms * 1e-3)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    it_s = sum(ran) / args.steps / (ms * 1e-3)
+    kinfo = k.info()
+    slots, narrow = int(kinfo.stored_slots), int(kinfo.narrow_slots)
     b_it = 12 * nnz + 104 * n + (12 * nnz + 24 * n) / 50
-    out = {
-        "metric": "CG iterations/s", "value": round(it_s, 2), "unit": "it/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config]["name"], "kernel": args.kernel, "permuted": args.permuted,
-                   "row_order": args.row_order, "iterations_per_step": iters, "nrows": n, "nnz": nnz,
-                   "stored_slots": k.stored_slots, "prepare_s": round(t_prepare, 3), "step_ms_rank0": step_ms, "step_host_ms_rank0": host},
-        "roofline": None,
-        "iteration_roofline": {"bound": "hbm", "achieved": round(b_it * it_s / world / 1e9, 1), "peak": hbm,
-                               "unit": "GB/s", "frac": round(b_it * it_s / world / 1e9 / hbm, 4),
-                               "algorithmic_bytes_per_iteration": b_it,
-                               "note": "12 nnz + 104 n + refresh share per iteration / iteration time"},
-        "gpu_launches": int(launches), "clocks": clk.summary(),
-    }
+    # the bytes the layout streams instead of 12 B/nnz (padding; 16-bit columns)
+    lay_bytes = 8 * slots + 2 * narrow + 4 * (slots - narrow)
+    s_it = b_it + (lay_bytes - 12 * nnz) * (1 + 1 / 50)
     # dominant kernel: the SpMV (~2/3 of an iteration), timed alone with CUDA
     # events on its stream, x (a CG direction) L2-resident as in the solve
     stream = torch.cuda.current_stream()
@@ -683,22 +742,79 @@ def run_cg(args, rank, world, local):
     e1.synchronize()
     t_k = e0.elapsed_time(e1) * 1e-3 / 50
     alg = 12 * nnz + 8 * n + 8 * nc
-    key = f"{args.config}/cg_k1_dot/{args.row_order}"
-    out["roofline"] = {"bound": "hbm", "achieved": round(alg / t_k / 1e9, 1), "peak": hbm, "peak_source": peak_src,
-                       "unit": "GB/s", "frac": round(alg / t_k / 1e9 / hbm, 4),
-                       "traffic": ncu_traffic(key) if args.scale == 1.0 else None,
-                       "traffic_source": f"profiles/ncu_traffic.json[{key}] (the CG's SpMV+p.q kernel)",
-                       "kernel": "k1_kernel", "kernel_us": round(t_k * 1e6, 2),
-                       "algorithmic_bytes_per_launch": alg}
+    key = f"{args.config}/cg_k1_dot/{row_order}"
     # end to end through ew_cg_solve[_permuted] with host b / diag / x
-    bh = np.ascontiguousarray(b)
     t = time.perf_counter()
-    for _ in range(max(1, min(args.steps, 2))):
-        k.cg_solve(bh, diag, tol=1e-300, max_iterations=iters, permuted=args.permuted)
-    e2e_s = (time.perf_counter() - t) / max(1, min(args.steps, 2))
-    out["e2e"] = {"value": round(iters / e2e_s, 2), "unit": "it/s", "h2d_bytes_per_step": 16 * n,
-                  "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
-                  "path": "ew_cg_solve_permuted(EW_MEM_HOST): b, diag in, solution + history out"}
+    reps = max(1, min(args.steps, 2))
+    for _ in range(reps):
+        r2 = k.cg_solve(b, diag, tol=1e-300, max_iterations=iters, permuted=permuted)
+        assert r2.iterations == iters
+    e2e_s = (time.perf_counter() - t) / reps
+    return {
+        "value": round(it_s, 2), "ms_per_step": round(ms, 4), "row_order": row_order,
+        "iterations_run": ran, "stored_slots": slots, "prepare_s": round(t_prepare, 3),
+        "step_ms": step_ms, "step_host_ms": host, "gpu_launches": int(launches), "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(alg / t_k / 1e9, 1), "peak": hbm, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": round(alg / t_k / 1e9 / hbm, 4),
+                     "streamed_frac": round((lay_bytes + 8 * n + 8 * nc) / t_k / 1e9 / hbm, 4),
+                     "traffic": ncu_traffic(key) if args.scale == 1.0 else None,
+                     "traffic_source": f"profiles/ncu_traffic.json[{key}] (the CG's SpMV+p.q kernel)",
+                     "kernel": "k1_kernel (apply_permuted)" if k.has_perm else "k1_kernel",
+                     "kernel_us": round(t_k * 1e6, 2), "algorithmic_bytes_per_launch": alg},
+        "iteration_roofline": {"bound": "hbm", "achieved": round(b_it * it_s / 1e9, 1), "peak": hbm,
+                               "unit": "GB/s", "frac": round(b_it * it_s / 1e9 / hbm, 4),
+                               "streamed_frac": round(s_it * it_s / 1e9 / hbm, 4),
+                               "algorithmic_bytes_per_iteration": b_it, "streamed_bytes_per_iteration": s_it,
+                               "note": "frac: 12 nnz + 104 n + refresh share per iteration / iteration time; "
+                                       "streamed_frac: the same with the layout's own matrix bytes (padding, "
+                                       "16-bit columns) in place of 12 B/nnz"},
+        "e2e": {"value": round(iters / e2e_s, 2), "unit": "it/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
+                "path": "ew_cg_solve_permuted(EW_MEM_HOST): b, diag in, solution + history out"},
+    }
+
+
+def run_cg(args, rank, world, local):
+    """Jacobi PCG on one GPU (config 4 by default): the kernel in the row
+    order(s) asked for, 1000 forced iterations per step."""
+    if world > 1 or args.config == "c5":
+        return run_cg_dist(args, rank, world, local, shape="c5")
+    import torch
+
+    from paper_1501_00324_b200 import capi
+
+    n, nc, ro, ci, v = build_matrix(args.config, args.scale)
+    nnz = int(ro[-1])
+    a = capi.Csr(n, nc, ro, ci, v)
+    diag = a.extract_diagonal()
+    b = a.spmv(np.ones(nc))  # b = A * 1 (ellwarp_cli.cpp:192-195)
+    bd = torch.tensor(b, device="cuda")
+    dd = torch.tensor(diag, device="cuda")
+    orders = [args.row_order]
+    if args.kernel.endswith(("r", "rs")) and args.both_orders:
+        orders = ["locality", "reference"] if args.row_order == "locality" else ["reference", "locality"]
+    lines = []
+    for order in orders:
+        lines.append(cg_one_gpu(args, a, n, nc, nnz, bd, dd, b, diag, args.kernel, order, local))
+        torch.cuda.empty_cache()
+    del a
+    first = lines[0]
+    out = {
+        "metric": "CG iterations/s", "value": first["value"], "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": first["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel,
+                   "row_order": first["row_order"], "iterations_per_step": args.iterations, "nrows": n,
+                   "nnz": nnz, "stored_slots": first["stored_slots"], "prepare_s": first["prepare_s"],
+                   "iterations_run": first["iterations_run"], "step_ms_rank0": first["step_ms"],
+                   "step_host_ms_rank0": first["step_host_ms"]},
+        "roofline": first["roofline"], "iteration_roofline": first["iteration_roofline"], "e2e": first["e2e"],
+        "gpu_launches": first["gpu_launches"], "clocks": first["clocks"],
+    }
+    for other in lines[1:]:
+        out[f"{other['row_order']}_row_order"] = {kk: other[kk] for kk in (
+            "value", "ms_per_step", "iterations_run", "stored_slots", "prepare_s", "step_ms", "roofline",
+            "iteration_roofline", "e2e", "gpu_launches", "clocks")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5full":
         rate, its, dt = reference_cg_rate(n, nc, ro, ci, v, iters=max(2, args.cpu_cg_iters))
         out["cpu_baseline"] = {"value": round(rate, 3), "unit": "it/s", "cores": 1, "kind": "reference",
@@ -946,7 +1062,10 @@ def main():
     p.add_argument("--cpu-cg-iters", type=int, default=20)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cg-steps", type=int, default=10,
-                   help="spmv workload: also time this many 1000-iteration partitioned CG steps (0: skip)")
+                   help="spmv workload: also time this many 1000-iteration CG steps of config 4 (N=1) and "
+                        "config 5 (partitioned over the N GPUs; at most 3 steps) (0: skip)")
+    p.add_argument("--both-orders", type=int, default=1,
+                   help="CG on an r / rs kernel: also time the other row order (reference / locality)")
     args = p.parse_args()
     args.warmup = max(3, args.warmup)
     if args.config is None:
@@ -974,22 +1093,31 @@ def main():
         return
     out = run_spmv(args, rank, world, local) if args.workload == "spmv" else run_cg(args, rank, world, local)
     if args.workload == "spmv" and args.cg_steps > 0:
-        # BASELINE.json's second metric beside the headline: the partitioned
-        # Jacobi PCG on a config-2-sized elasticity slab per GPU (weak scaling,
-        # the same path at every N, 1000 iterations per step)
+        # BASELINE.json's second metric beside the headline: CG iterations/s
+        # on config 4 (one GPU, N=1 only) and on config 5 partitioned over
+        # the N GPUs (the same 100M-row mesh at every N: strong scaling)
         import gc
 
         import torch
 
+        keys = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "scaling", "config",
+                "roofline", "iteration_roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline",
+                "reference_row_order")
+        if world == 1:
+            gc.collect()
+            torch.cuda.empty_cache()
+            c4 = argparse.Namespace(**vars(args))
+            c4.steps, c4.workload, c4.config, c4.kernel = args.cg_steps, "cg", "c4", "k1rs"
+            c4.permuted, c4.row_order, c4.warmup = True, "locality", 3
+            line = run_cg(c4, rank, world, local)
+            out["cg_c4"] = {kk: line[kk] for kk in keys if kk in line}
         gc.collect()
         torch.cuda.empty_cache()
-        cg_args = argparse.Namespace(**vars(args))
-        cg_args.steps, cg_args.workload = args.cg_steps, "cg"
-        cg = run_cg_dist(cg_args, rank, world, local)
+        c5 = argparse.Namespace(**vars(args))
+        c5.steps, c5.workload, c5.warmup = min(3, args.cg_steps), "cg", 1
+        cg = run_cg_dist(c5, rank, world, local, shape="c5")
         if rank == 0:
-            out["cg"] = {key: cg[key] for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup",
-                                                   "ms_per_step", "scaling", "config", "roofline", "e2e",
-                                                   "gpu_launches", "clocks")}
+            out["cg"] = {kk: cg[kk] for kk in keys if kk in cg}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -349,6 +349,107 @@ void ewo_spmv_layout(const ewo_layout* l, const double* x, int scatter, double* 
     free(acc);
 }
 
+/* ewo_spmv_layout restricted to the warps [w0, w1): writes every row those
+ * warps hold (0.0 for rows without entries), the same per-lane arithmetic.
+ * Warps own disjoint rows, so ranges can run on separate threads. */
+static void spmv_layout_warps(const ewo_layout* l, const double* x, int scatter, double* y, int64_t w0,
+                              int64_t w1, double* acc) {
+    const int64_t ws = l->warp_size;
+    for (int64_t w = w0; w < w1; ++w) {
+        const int64_t red = l->kind == 2 ? l->reduction[w] : 1;
+        const int64_t first = l->kind == 2 ? l->rows_offset_warp[w] : w * ws;
+        const int64_t mx = l->maxrows[w];
+        for (int64_t r = 0; r < l->rows_in_warp[w]; ++r) {
+            const int64_t pos = first + r;
+            double* out = &y[scatter ? l->forward[pos] : pos];
+            if (l->sorted_row_length[pos] == 0) {
+                *out = 0.0;
+                continue;
+            }
+            for (int64_t t = 0; t < red; ++t) {
+                const int64_t lane = r * red + t;
+                double s = 0.0;
+                for (int64_t j = 0; j < mx; ++j) {
+                    const int64_t k = slot_of(l, w, lane, j);
+                    s += l->values[k] * x[l->col_indices[k]];
+                }
+                acc[lane] = s;
+            }
+            for (int64_t stride = 1; stride < red; stride <<= 1)
+                for (int64_t t = 0; t + stride < red; t += 2 * stride)
+                    acc[r * red + t] += acc[r * red + t + stride];
+            *out = acc[r * red];
+        }
+    }
+}
+
+/* Fork-join over [0, n) in `threads` contiguous ranges (a fresh pthread per
+ * range; the caller's thread takes the first). */
+typedef void (*range_fn)(void* ctx, int64_t i0, int64_t i1);
+typedef struct {
+    range_fn fn;
+    void* ctx;
+    int64_t i0, i1;
+} range_job;
+
+static void* range_main(void* a) {
+    range_job* j = (range_job*)a;
+    j->fn(j->ctx, j->i0, j->i1);
+    return NULL;
+}
+
+static void par_for(int threads, int64_t n, range_fn fn, void* ctx) {
+    if (threads <= 1 || n < 4096) {
+        fn(ctx, 0, n);
+        return;
+    }
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    range_job job[256];
+    int started[256];
+    const int64_t chunk = (n + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+        job[t].fn = fn;
+        job[t].ctx = ctx;
+        job[t].i0 = t * chunk < n ? t * chunk : n;
+        job[t].i1 = (t + 1) * chunk < n ? (t + 1) * chunk : n;
+        started[t] = 0;
+    }
+    for (int t = 1; t < threads; ++t)
+        started[t] = pthread_create(&tid[t], NULL, range_main, &job[t]) == 0;
+    fn(ctx, job[0].i0, job[0].i1);
+    for (int t = 1; t < threads; ++t) {
+        if (started[t])
+            pthread_join(tid[t], NULL);
+        else
+            fn(ctx, job[t].i0, job[t].i1);  /* no thread: run the range here */
+    }
+}
+
+typedef struct {
+    const ewo_layout* l;
+    const double* x;
+    double* y;
+    int scatter;
+} layout_range_ctx;
+
+static void layout_range(void* c, int64_t w0, int64_t w1) {
+    const layout_range_ctx* lc = (const layout_range_ctx*)c;
+    double* acc = (double*)malloc(sizeof(double) * (size_t)lc->l->warp_size);
+    spmv_layout_warps(lc->l, lc->x, lc->scatter, lc->y, w0, w1, acc);
+    free(acc);
+}
+
+void ewo_spmv_layout_mt(const ewo_layout* l, const double* x, int scatter, double* y, int threads) {
+    layout_range_ctx c = {l, x, y, scatter};
+    par_for(threads, l->nwarps, layout_range, &c);
+}
+
+void ewo_layout_op_mt(void* ctx, const double* x, double* y) {
+    const ewo_layout_mt_ctx* c = (const ewo_layout_mt_ctx*)ctx;
+    ewo_spmv_layout_mt(c->l, x, c->scatter, y, c->threads);
+}
+
 /* reorder.cpp:8-43: columns renumbered by inverse; for rs each row's
  * (column, value) pairs are re-sorted by the new column (keys are unique
  * because renumbering is a bijection). */
@@ -394,9 +495,87 @@ static int all_finite(int64_t n, const double* v) {
     return 1;
 }
 
+/* The CG's element-wise loops (each element's arithmetic exactly as in
+ * cg.cpp; elements are independent, so ranges may run on threads). */
+enum { EW_RESID, EW_PRECOND, EW_PRECOND_P, EW_XR, EW_PUPD, EW_FINITE };
+typedef struct {
+    int what, jacobi;
+    const double *b, *diag, *q;
+    double *x, *r, *z, *p;
+    double alpha, beta;
+    int bad[256];
+    int64_t chunk;
+} vec_ctx;
+
+static void vec_range(void* c, int64_t i0, int64_t i1) {
+    vec_ctx* v = (vec_ctx*)c;
+    switch (v->what) {
+        case EW_RESID: /* cg.cpp:58, 85 */
+            for (int64_t i = i0; i < i1; ++i) v->r[i] = v->b[i] - v->q[i];
+            break;
+        case EW_PRECOND: /* cg.cpp:36-42, 96 */
+        case EW_PRECOND_P: /* + cg.cpp:67 p = z */
+            for (int64_t i = i0; i < i1; ++i) {
+                v->z[i] = v->jacobi ? v->r[i] / v->diag[i] : v->r[i];
+                if (v->what == EW_PRECOND_P) v->p[i] = v->z[i];
+            }
+            break;
+        case EW_XR: /* cg.cpp:78-81 */
+            for (int64_t i = i0; i < i1; ++i) {
+                v->x[i] += v->alpha * v->p[i];
+                v->r[i] -= v->alpha * v->q[i];
+            }
+            break;
+        case EW_PUPD: /* cg.cpp:99 */
+            for (int64_t i = i0; i < i1; ++i) v->p[i] = v->z[i] + v->beta * v->p[i];
+            break;
+        case EW_FINITE: /* cg.cpp:87 */
+            for (int64_t i = i0; i < i1; ++i)
+                if (!isfinite(v->r[i])) {
+                    v->bad[v->chunk ? i0 / v->chunk : 0] = 1;
+                    break;
+                }
+            break;
+    }
+}
+
+static void vec_op(vec_ctx* v, int what, int threads, int64_t n) {
+    v->what = what;
+    par_for(threads, n, vec_range, v);
+}
+
+static int vec_finite(vec_ctx* v, int threads, int64_t n) {
+    int t = threads <= 1 || n < 4096 ? 1 : (threads > 256 ? 256 : threads);
+    memset(v->bad, 0, sizeof(v->bad));
+    v->chunk = (n + t - 1) / t;
+    vec_op(v, EW_FINITE, threads, n);
+    for (int i = 0; i < 256; ++i)
+        if (v->bad[i]) return 0;
+    return 1;
+}
+
+static int cg_core(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const double* diag,
+                   const ewo_cg_config* cfg, double* x, double* history, ewo_cg_result* res,
+                   int threads);
+
 /* cg.cpp:25-104 */
 int ewo_cg_solve(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const double* diag,
                  const ewo_cg_config* cfg, double* x, double* history, ewo_cg_result* res) {
+    return cg_core(op, ctx, n, b, diag, cfg, x, history, res, 1);
+}
+
+/* The same solve with the element-wise loops on `threads` threads; every
+ * dot product stays the reference's sequential sum (cg.cpp:9-13), so the
+ * history is bit-identical to ewo_cg_solve with the same operator. */
+int ewo_cg_solve_mt(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const double* diag,
+                    const ewo_cg_config* cfg, double* x, double* history, ewo_cg_result* res,
+                    int threads) {
+    return cg_core(op, ctx, n, b, diag, cfg, x, history, res, threads);
+}
+
+static int cg_core(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const double* diag,
+                   const ewo_cg_config* cfg, double* x, double* history, ewo_cg_result* res,
+                   int threads) {
     memset(res, 0, sizeof(*res));
     if (!(cfg->rel_tolerance > 0.0)) return 1;
     if (!all_finite(n, b)) return 2;
@@ -419,17 +598,26 @@ int ewo_cg_solve(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const do
     double* p = (double*)malloc(sizeof(double) * (size_t)(n + 1));
     double* q = (double*)malloc(sizeof(double) * (size_t)(n + 1));
     int status = 0;
+    vec_ctx vc;
+    memset(&vc, 0, sizeof(vc));
+    vc.jacobi = jacobi;
+    vc.b = b;
+    vc.diag = diag;
+    vc.q = q;
+    vc.x = x;
+    vc.r = r;
+    vc.z = z;
+    vc.p = p;
     op(ctx, x, q);
     res->spmv_calls++;
-    for (int64_t i = 0; i < n; ++i) r[i] = b[i] - q[i];
+    vec_op(&vc, EW_RESID, threads, n);
     int64_t h = 0;
     history[h++] = sqrt(dot(n, r, r)) / bnorm;
     if (history[0] <= cfg->rel_tolerance) {
         res->converged = 1;
         goto done;
     }
-    for (int64_t i = 0; i < n; ++i) z[i] = jacobi ? r[i] / diag[i] : r[i];
-    memcpy(p, z, sizeof(double) * (size_t)n);
+    vec_op(&vc, EW_PRECOND_P, threads, n);
     double rz = dot(n, r, z);
     for (int64_t k = 1; k <= cfg->max_iterations; ++k) {
         op(ctx, p, q);
@@ -440,16 +628,14 @@ int ewo_cg_solve(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const do
             goto done;
         }
         const double alpha = rz / pq;
-        for (int64_t i = 0; i < n; ++i) {
-            x[i] += alpha * p[i];
-            r[i] -= alpha * q[i];
-        }
+        vc.alpha = alpha;
+        vec_op(&vc, EW_XR, threads, n);
         if (cfg->recompute_interval > 0 && k % cfg->recompute_interval == 0) {
             op(ctx, x, q);
             res->spmv_calls++;
-            for (int64_t i = 0; i < n; ++i) r[i] = b[i] - q[i];
+            vec_op(&vc, EW_RESID, threads, n);
         }
-        if (!all_finite(n, r)) {
+        if (!vec_finite(&vc, threads, n)) {
             status = 2;
             goto done;
         }
@@ -464,10 +650,11 @@ int ewo_cg_solve(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const do
             res->converged = 1;
             goto done;
         }
-        for (int64_t i = 0; i < n; ++i) z[i] = jacobi ? r[i] / diag[i] : r[i];
+        vec_op(&vc, EW_PRECOND, threads, n);
         const double rz_new = dot(n, r, z);
         const double beta = rz_new / rz;
-        for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        vc.beta = beta;
+        vec_op(&vc, EW_PUPD, threads, n);
         rz = rz_new;
     }
     res->converged = 0;
@@ -510,8 +697,19 @@ void ewo_layout_op(void* ctx, const double* x, double* y) {
 int ewo_cg_layout(const ewo_layout* l, int permuted, int64_t n, const double* b,
                   const double* diag, const ewo_cg_config* cfg, double* x, double* history,
                   ewo_cg_result* res) {
-    ewo_layout_ctx ctx = {l, permuted ? 0 : 1};
-    if (!permuted) return ewo_cg_solve(ewo_layout_op, &ctx, n, b, diag, cfg, x, history, res);
+    return ewo_cg_layout_mt(l, permuted, n, b, diag, cfg, x, history, res, 1);
+}
+
+/* ewo_cg_layout with the layout SpMV split over warps and the element-wise
+ * loops over rows on `threads` threads: each row's sum and each dot product
+ * are the single-threaded ones, so results are bit-identical for any thread
+ * count (the config-4 parity check runs 1000+ iterations of 5M rows). */
+int ewo_cg_layout_mt(const ewo_layout* l, int permuted, int64_t n, const double* b,
+                     const double* diag, const ewo_cg_config* cfg, double* x, double* history,
+                     ewo_cg_result* res, int threads) {
+    ewo_layout_mt_ctx ctx = {l, permuted ? 0 : 1, threads};
+    if (!permuted)
+        return ewo_cg_solve_mt(ewo_layout_op_mt, &ctx, n, b, diag, cfg, x, history, res, threads);
     double* bp = (double*)malloc(sizeof(double) * (size_t)(n + 1));
     double* dp = diag ? (double*)malloc(sizeof(double) * (size_t)(n + 1)) : NULL;
     double* xp = (double*)malloc(sizeof(double) * (size_t)(n + 1));
@@ -519,7 +717,7 @@ int ewo_cg_layout(const ewo_layout* l, int permuted, int64_t n, const double* b,
         bp[k] = b[l->forward[k]];
         if (dp) dp[k] = diag[l->forward[k]];
     }
-    const int st = ewo_cg_solve(ewo_layout_op, &ctx, n, bp, dp, cfg, xp, history, res);
+    const int st = ewo_cg_solve_mt(ewo_layout_op_mt, &ctx, n, bp, dp, cfg, xp, history, res, threads);
     for (int64_t k = 0; k < n; ++k) x[l->forward[k]] = xp[k];
     free(bp);
     free(dp);

@@ -119,6 +119,19 @@ typedef struct {
     int scatter;
 } ewo_layout_ctx;
 void ewo_layout_op(void* ctx, const double* x, double* y);
+/* Multi-threaded forms for full-size parity runs: warps (SpMV) and rows
+ * (CG vector updates) split over threads, dot products sequential; bitwise
+ * equal to the single-threaded functions for any thread count. */
+typedef struct {
+    const ewo_layout* l;
+    int scatter;
+    int threads;
+} ewo_layout_mt_ctx;
+void ewo_layout_op_mt(void* ctx, const double* x, double* y);
+void ewo_spmv_layout_mt(const ewo_layout* l, const double* x, int scatter, double* y, int threads);
+int ewo_cg_solve_mt(ewo_spmv_fn op, void* ctx, int64_t n, const double* b, const double* diag,
+                    const ewo_cg_config* cfg, double* x, double* history, ewo_cg_result* res,
+                    int threads);
 
 /* One CG over csr / layout operators chosen by id, as the reference's
  * _ellwarp.cg_solve binding does (module.cpp:227-249); permuted selects
@@ -126,6 +139,9 @@ void ewo_layout_op(void* ctx, const double* x, double* y);
 int ewo_cg_layout(const ewo_layout* l, int permuted, int64_t n, const double* b,
                   const double* diag, const ewo_cg_config* cfg, double* x, double* history,
                   ewo_cg_result* res);
+int ewo_cg_layout_mt(const ewo_layout* l, int permuted, int64_t n, const double* b,
+                     const double* diag, const ewo_cg_config* cfg, double* x, double* history,
+                     ewo_cg_result* res, int threads);
 
 #ifdef __cplusplus
 }

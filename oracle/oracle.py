@@ -149,6 +149,8 @@ class Restatement:
         L.ewo_value_slot_map.argtypes = [C.POINTER(_Layout), _i64p, _i64p]
         L.ewo_cg_layout.argtypes = [C.POINTER(_Layout), C.c_int, C.c_int64, _f64p, _f64p,
                                     C.POINTER(_CgCfg), _f64p, _f64p, C.POINTER(_CgRes)]
+        L.ewo_cg_layout_mt.argtypes = L.ewo_cg_layout.argtypes + [C.c_int]
+        L.ewo_spmv_layout_mt.argtypes = [C.POINTER(_Layout), _f64p, C.c_int, _f64p, C.c_int]
         L.ewo_cg_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, _f64p, _f64p,
                                    C.POINTER(_CgCfg), _f64p, _f64p, C.POINTER(_CgRes)]
         L.ewo_compute_k2_lanes.argtypes = [C.c_int64, C.c_int64, C.c_int64]
@@ -248,10 +250,15 @@ class Restatement:
             self.lib.ewo_layout_free(lay._ptr)
             lay._ptr = None
 
-    def spmv_layout(self, lay: Layout, x, scatter=True):
+    def spmv_layout(self, lay: Layout, x, scatter=True, threads=1):
+        """run_k1 / run_k2; threads > 1 splits the warps over host threads
+        (same per-lane sums: bitwise the single-threaded result)."""
         x = np.ascontiguousarray(x, np.float64)
         y = np.empty(lay.nrows, np.float64)
-        self.lib.ewo_spmv_layout(lay._ptr, _fp(x), int(scatter), _fp(y))
+        if threads > 1:
+            self.lib.ewo_spmv_layout_mt(lay._ptr, _fp(x), int(scatter), _fp(y), int(threads))
+        else:
+            self.lib.ewo_spmv_layout(lay._ptr, _fp(x), int(scatter), _fp(y))
         return y
 
     def value_slot_map(self, lay: Layout, m: Csr):
@@ -296,13 +303,16 @@ class Restatement:
             C.byref(cfg), _fp(x), _fp(h), C.byref(r)), m.nrows, max_iterations)
 
     def cg_layout(self, lay: Layout, b, diag=None, permuted=False, tol=1e-8, max_iterations=1000,
-                  jacobi=True, recompute=50, divergence=1e6):
+                  jacobi=True, recompute=50, divergence=1e6, threads=1):
+        """cg_solve / cg_solve_permuted over a layout operator. threads > 1:
+        SpMV warps and vector updates on host threads, every dot product the
+        reference's sequential sum -- bitwise the single-threaded history."""
         b = np.ascontiguousarray(b, np.float64)
         d = np.ascontiguousarray(diag, np.float64) if diag is not None else None
         cfg = _cg_cfg(tol, max_iterations, jacobi, recompute, divergence)
-        return self._cg(lambda x, h, r: self.lib.ewo_cg_layout(
+        return self._cg(lambda x, h, r: self.lib.ewo_cg_layout_mt(
             lay._ptr, int(permuted), lay.nrows, _fp(b), _fp(d) if d is not None else None,
-            C.byref(cfg), _fp(x), _fp(h), C.byref(r)), lay.nrows, max_iterations)
+            C.byref(cfg), _fp(x), _fp(h), C.byref(r), int(threads)), lay.nrows, max_iterations)
 
     def compute_alpha(self, tr, tk, tb):
         a = C.c_int64()

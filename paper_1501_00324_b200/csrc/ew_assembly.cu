@@ -281,7 +281,6 @@ __global__ void compose_kernel(const int64_t* __restrict__ slot_map, const int64
 // (pattern entry k -> the slot its value occupies), residual as usual.
 void assembly_run_into(const AssemblyData& A, const double* ke, const double* re, KernelData& k, double* residual,
                        cudaStream_t s) {
-    drop_host_pipeline(k);  // the tangent replaces the layout's values
     require(k.layout && !k.format, "assembly: the kernel must be an ELL-WARP (k1 / k2 family) kernel");
     require(k.nrows == A.nnodes && k.nnz == A.nnz, "assembly: the kernel was not prepared on the assembly pattern");
     LayoutData& l = *k.layout;

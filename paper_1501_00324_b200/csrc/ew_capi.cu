@@ -504,7 +504,6 @@ ew_status ew_kernel_refresh_values(ew_kernel k, ew_csr m, void* stream) {
         auto& d = *k->d;
         const cudaStream_t s = ew::as_stream(stream);
         ew::require(m->d->nrows == d.nrows && m->d->nnz == d.nnz, "refresh: structure mismatch");
-        ew::drop_host_pipeline(d);  // its block layouts hold the old values
         if (d.format && (d.format->kind == ew::FormatData::kEll || d.format->kind == ew::FormatData::kHyb))
             throw ew::Error(EW_UNSUPPORTED, "values-only refresh of ell/hyb kernels is not implemented");
         if (d.csr) {

@@ -26,6 +26,8 @@
 //    the process uses the same NCCL torch.distributed loaded);
 //  * copy: all partitions in this process on the current device, halos as
 //    device-to-device copies (tests the partitioned algorithm on 1 GPU).
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -292,22 +294,21 @@ __global__ void halo_wait_kernel(uint64_t* mine, int G, const int32_t* __restric
 // every partition's mailbox (its own included), then the flag.
 __global__ void publish_kernel(const cg::State* st, uint64_t* const* mboxes, int me, int G, const uint64_t* epochs) {
     const uint64_t epoch = epochs[1] + 1;  // this reduction (the collect kernel advances the counter)
-    const int g = threadIdx.x;
-    if (g >= G) return;
-    uint64_t* mb = mboxes[g];
-    double* v = reinterpret_cast<double*>(mb + Mbox::val(G, me, epoch));
-    v[0] = st->loc[0];
-    v[1] = st->loc[1];
-    __threadfence_system();
-    st_release_sys(mb + Mbox::red(G, me), epoch);
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {  // any G, not just one warp's worth
+        uint64_t* mb = mboxes[g];
+        double* v = reinterpret_cast<double*>(mb + Mbox::val(G, me, epoch));
+        v[0] = st->loc[0];
+        v[1] = st->loc[1];
+        __threadfence_system();
+        st_release_sys(mb + Mbox::red(G, me), epoch);
+    }
 }
 
 // Reduction, step 2: wait for every partition's totals, copy them to
 // `gathered` in rank order (then cg::finalize_kernel sums them).
 __global__ void collect_kernel(uint64_t* mine, int G, uint64_t* epochs, double* gathered) {
     const uint64_t epoch = epochs[1] + 1;
-    const int g = threadIdx.x;
-    if (g < G) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
         spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
         const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
         gathered[2 * g] = ld_relaxed_sys(v);
@@ -322,8 +323,7 @@ __global__ void collect_kernel(uint64_t* mine, int G, uint64_t* epochs, double* 
 __global__ void collect_finalize_kernel(uint64_t* mine, int G, uint64_t* epochs, double* gathered, int what,
                                         double tol, double divergence, cg::State* st, double* hist) {
     const uint64_t epoch = epochs[1] + 1;
-    const int g = threadIdx.x;
-    if (g < G) {
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
         spin_until(mine + Mbox::red(G, g), epoch, mine + Mbox::err(G));
         const double* v = reinterpret_cast<const double*>(mine + Mbox::val(G, g, epoch));
         gathered[2 * g] = ld_relaxed_sys(v);
@@ -362,36 +362,217 @@ bool split_rows(const std::string& kid, int32_t G) {
     return on && G > 1 && kid == "k1";
 }
 
-// K1 kernel over a subset of the local rows (ascending local ids), entries
-// in their order, its layout scattering into local row ids.
-std::shared_ptr<KernelData> prepare_rows(const std::vector<int64_t>& rows, const std::vector<int64_t>& lro,
-                                         const std::vector<int64_t>& lci, const double* lv, int64_t ncols,
+// ---- partition build on the device -------------------------------------------
+// The block's CSR goes up once; local column numbering, the interior /
+// boundary row split and the row subsets are device passes, so the host holds
+// nothing beyond the caller's arrays (config 5 on one GPU: 4.5G entries).
+
+// Global -> local column ids: owned c - r0, ghosts nloc + rank in gh (sorted).
+__global__ void localize_kernel(const int64_t* __restrict__ cg, int64_t n, int64_t r0, int64_t r1, int64_t nloc,
+                                const int64_t* __restrict__ gh, int64_t ngh, int32_t* __restrict__ out, int* bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t c = cg[i];
+    if (c >= r0 && c < r1) {
+        out[i] = static_cast<int32_t>(c - r0);
+        return;
+    }
+    int64_t lo = 0, hi = ngh;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (gh[mid] < c) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo == ngh || gh[lo] != c) {
+        atomicOr(bad, 1);
+        out[i] = 0;
+        return;
+    }
+    out[i] = static_cast<int32_t>(nloc + lo);
+}
+
+// Row offsets rebased to 0, per-row checks, the longest row and whether a
+// row reads a ghost column.
+__global__ void local_rows_kernel(int64_t* __restrict__ ro, int64_t base, const int32_t* __restrict__ ci,
+                                  int64_t nloc, int64_t nnz, uint8_t* __restrict__ has_ghost, int* maxrow,
+                                  int* bad) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nloc) return;
+    const int64_t lo = ro[r] - base, hi = ro[r + 1] - base;
+    if (lo > hi || lo < 0 || hi > nnz) {
+        atomicOr(bad, 2);
+        has_ghost[r] = 0;
+        return;
+    }
+    bool g = false;
+    for (int64_t k = lo; k < hi && !g; ++k) g = ci[k] >= nloc;
+    has_ghost[r] = g;
+    atomicMax(maxrow, static_cast<int>(hi - lo > 0x7fffffff ? 0x7fffffff : hi - lo));
+}
+
+__global__ void rebase_kernel(int64_t* __restrict__ ro, int64_t n, int64_t base) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) ro[r] -= base;
+}
+
+__global__ void sel_len_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ rows, int64_t n,
+                               int64_t* __restrict__ len) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) len[i] = ro[rows[i] + 1] - ro[rows[i]];
+}
+
+// Entries of the selected rows, one warp per row (coalesced row copies).
+__global__ void sel_copy_kernel(const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, const int32_t* __restrict__ rows, int64_t n,
+                                const int64_t* __restrict__ sro, int32_t* __restrict__ sci, double* __restrict__ sv) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int64_t a = ro[rows[i]], len = ro[rows[i] + 1] - a, d = sro[i];
+    for (int64_t k = lane; k < len; k += 32) {
+        sci[d + k] = ci[a + k];
+        sv[d + k] = v[a + k];
+    }
+}
+
+// Layout row permutation of a row subset back to local row ids.
+__global__ void remap_rows_kernel(int32_t* __restrict__ f, const int32_t* __restrict__ rows, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) f[i] = rows[f[i]];
+}
+
+// The block's rows [r0, r1) with local columns: bro = the rows' offsets into
+// bci / bv (any base), bci global column ids. has_ghost receives the row flags.
+std::shared_ptr<CsrData> upload_local(int64_t nloc, int64_t nghost, const int64_t* bro, const int64_t* bci,
+                                      const double* bv, int64_t r0, int64_t r1, const std::vector<int64_t>& ghosts,
+                                      DevBuf<uint8_t>& has_ghost, cudaStream_t s) {
+    auto m = std::make_shared<CsrData>();
+    const int64_t base = bro[0], nnz = bro[nloc] - bro[0];
+    require(nnz >= 0, "partition: row offsets decrease");
+    m->nrows = nloc;
+    m->ncols = nloc + nghost;
+    m->nnz = nnz;
+    if (m->ncols > 0x7fffffff) throw Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 local columns");
+    m->ro.alloc(nloc + 1);
+    m->ci.alloc(nnz);
+    m->v.alloc(nnz);
+    EW_CUDA_CHECK(cudaMemcpyAsync(m->ro.get(), bro, (nloc + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (nnz) EW_CUDA_CHECK(cudaMemcpyAsync(m->v.get(), bv + base, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+    DevBuf<int64_t> gh(ghosts.size());
+    if (!ghosts.empty())
+        EW_CUDA_CHECK(cudaMemcpyAsync(gh.get(), ghosts.data(), ghosts.size() * 8, cudaMemcpyHostToDevice, s));
+    Scratch<int> flags(2, s);
+    EW_CUDA_CHECK(cudaMemsetAsync(flags.get(), 0, 2 * sizeof(int), s));
+    constexpr int64_t kChunk = int64_t{1} << 27;  // 1 GB of int64 column ids per pass
+    if (nnz) {
+        Scratch<int64_t> cg(std::min(nnz, kChunk), s);
+        for (int64_t off = 0; off < nnz; off += kChunk) {
+            const int64_t cnt = std::min(kChunk, nnz - off);
+            EW_CUDA_CHECK(cudaMemcpyAsync(cg.get(), bci + base + off, cnt * 8, cudaMemcpyHostToDevice, s));
+            localize_kernel<<<grid_for(cnt), kBlock, 0, s>>>(cg.get(), cnt, r0, r1, nloc, gh.get(),
+                                                             static_cast<int64_t>(ghosts.size()), m->ci.get() + off,
+                                                             flags.get());
+            launched("localize_kernel");
+        }
+    }
+    has_ghost.alloc(std::max<int64_t>(1, nloc));
+    if (nloc) {
+        local_rows_kernel<<<grid_for(nloc), kBlock, 0, s>>>(m->ro.get(), base, m->ci.get(), nloc, nnz,
+                                                            has_ghost.get(), flags.get() + 1, flags.get());
+        launched("local_rows_kernel");
+        if (base) {
+            rebase_kernel<<<grid_for(nloc + 1), kBlock, 0, s>>>(m->ro.get(), nloc + 1, base);
+            launched("rebase_kernel");
+        }
+    }
+    int h[2];
+    EW_CUDA_CHECK(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    require(!(h[0] & 2), "row_offsets not nondecreasing");
+    require(!(h[0] & 1), "partition: a column is neither owned nor in the ghost list");
+    m->maxrow = h[1];
+    return m;
+}
+
+// Rows `rows` (device, ascending local ids) of m as their own CSR.
+std::shared_ptr<CsrData> select_rows(const CsrData& m, const int32_t* rows, int64_t n, cudaStream_t s) {
+    auto sub = std::make_shared<CsrData>();
+    sub->nrows = n;
+    sub->ncols = m.ncols;
+    sub->maxrow = m.maxrow;
+    sub->ro.alloc(n + 1);
+    EW_CUDA_CHECK(cudaMemsetAsync(sub->ro.get(), 0, sizeof(int64_t), s));
+    if (n) {
+        Scratch<int64_t> len(n, s);
+        sel_len_kernel<<<grid_for(n), kBlock, 0, s>>>(m.ro.get(), rows, n, len.get());
+        launched("sel_len_kernel");
+        size_t bytes = 0;
+        EW_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, bytes, len.get(), sub->ro.get() + 1, n, s));
+        Scratch<unsigned char> tmp(bytes, s);
+        EW_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, len.get(), sub->ro.get() + 1, n, s));
+        launched("cub::DeviceScan::InclusiveSum");
+    }
+    EW_CUDA_CHECK(cudaMemcpyAsync(&sub->nnz, sub->ro.get() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    sub->ci.alloc(sub->nnz);
+    sub->v.alloc(sub->nnz);
+    if (n) {
+        sel_copy_kernel<<<grid_for(n * 32), kBlock, 0, s>>>(m.ro.get(), m.ci.get(), m.v.get(), rows, n,
+                                                            sub->ro.get(), sub->ci.get(), sub->v.get());
+        launched("sel_copy_kernel");
+    }
+    return sub;
+}
+
+// ids[i] = i; flag[i] = has_ghost[i] == want
+__global__ void row_sel_kernel(const uint8_t* __restrict__ has_ghost, int64_t n, uint8_t want,
+                               int32_t* __restrict__ ids, uint8_t* __restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ids[i] = static_cast<int32_t>(i);
+    flag[i] = (has_ghost[i] != 0) == (want != 0);
+}
+
+// Local row ids with has_ghost == want (ascending), on the device.
+int64_t flagged_rows(const DevBuf<uint8_t>& has_ghost, int64_t nloc, bool want, DevBuf<int32_t>& out, cudaStream_t s) {
+    out.alloc(std::max<int64_t>(1, nloc));
+    if (!nloc) return 0;
+    Scratch<int64_t> cnt(1, s);
+    Scratch<int32_t> ids(nloc, s);
+    Scratch<uint8_t> flag(nloc, s);
+    row_sel_kernel<<<grid_for(nloc), kBlock, 0, s>>>(has_ghost.get(), nloc, want ? 1 : 0, ids.get(), flag.get());
+    launched("row_sel_kernel");
+    size_t bytes = 0;
+    EW_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, bytes, ids.get(), flag.get(), out.get(), cnt.get(), nloc, s));
+    Scratch<unsigned char> tmp(bytes, s);
+    EW_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.get(), bytes, ids.get(), flag.get(), out.get(), cnt.get(), nloc, s));
+    launched("cub::DeviceSelect::Flagged");
+    int64_t n = 0;
+    EW_CUDA_CHECK(cudaMemcpyAsync(&n, cnt.get(), sizeof(n), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    return n;
+}
+
+// K1 kernel over the local rows `rows` (device, ascending), entries in their
+// order, its layout scattering into local row ids.
+std::shared_ptr<KernelData> prepare_rows(const CsrData& local, const DevBuf<int32_t>& rows, int64_t n,
                                          const std::string& kid, const ew_warp_config& cfg,
                                          const ew_kernel_options& opts, cudaStream_t s) {
-    const int64_t n = static_cast<int64_t>(rows.size());
-    std::vector<int64_t> sro(n + 1, 0), sci;
-    std::vector<double> sv;
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t r = rows[i];
-        sci.insert(sci.end(), lci.begin() + lro[r], lci.begin() + lro[r + 1]);
-        sv.insert(sv.end(), lv + lro[r], lv + lro[r + 1]);
-        sro[i + 1] = static_cast<int64_t>(sci.size());
-    }
-    auto sub = csr_upload(n, ncols, n + 1, sro.data(), static_cast<int64_t>(sci.size()), sci.data(), sv.data(),
-                          EW_MEM_HOST, false, s);
-    auto k = prepare(kid, *sub, cfg, opts, s);
-    if (n) {
-        std::vector<int32_t> f(static_cast<size_t>(n));
-        EW_CUDA_CHECK(cudaMemcpyAsync(f.data(), k->layout->fwd.get(), n * 4, cudaMemcpyDeviceToHost, s));
+    std::shared_ptr<KernelData> k;
+    {
+        auto sub = select_rows(local, rows.get(), n, s);
+        k = prepare(kid, *sub, cfg, opts, s);
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
-        for (auto& v : f) v = static_cast<int32_t>(rows[v]);
-        EW_CUDA_CHECK(cudaMemcpyAsync(k->layout->fwd.get(), f.data(), n * 4, cudaMemcpyHostToDevice, s));
+    }
+    if (n) {
+        remap_rows_kernel<<<grid_for(n), kBlock, 0, s>>>(k->layout->fwd.get(), rows.get(), n);
+        launched("remap_rows_kernel");
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
     }
     return k;
 }
 
-// Partition g from its row block (bro: offsets relative to the block,
+// Partition g from its row block (bro: the rows' offsets into bci / bv,
 // bci: global column ids, bv: values), its ghost list and, per peer, the
 // global ids that peer needs from this partition (ascending).
 void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& bounds, const int64_t* bro,
@@ -415,31 +596,26 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
         }
         P.send_off[h + 1] = static_cast<int64_t>(sidx.size());
     }
-    // local CSR: owned columns c - r0, ghosts nloc + their position in `ghosts`
-    const int64_t lnnz = bro[P.nloc] - bro[0];
-    std::vector<int64_t> lro(P.nloc + 1), lci(lnnz);
-    for (int64_t r = 0; r <= P.nloc; ++r) lro[r] = bro[r] - bro[0];
-    for (int64_t k = 0; k < lnnz; ++k) {
-        const int64_t c = bci[bro[0] + k];
-        lci[k] = (c >= P.r0 && c < P.r1) ? c - P.r0
-                                         : P.nloc + (std::lower_bound(ghosts.begin(), ghosts.end(), c) - ghosts.begin());
-    }
+    // local CSR on the device: owned columns c - r0, ghosts nloc + their
+    // position in `ghosts`
+    DevBuf<uint8_t> has_ghost;
+    auto local = upload_local(P.nloc, P.nghost, bro, bci, bv, P.r0, P.r1, ghosts, has_ghost, s);
     if (split_rows(kid, G)) {
-        std::vector<int64_t> rows_int, rows_bnd;
-        for (int64_t r = 0; r < P.nloc; ++r) {
-            bool ghost = false;
-            for (int64_t k = lro[r]; k < lro[r + 1] && !ghost; ++k) ghost = lci[k] >= P.nloc;
-            (ghost ? rows_bnd : rows_int).push_back(r);
-        }
-        P.n_int = static_cast<int64_t>(rows_int.size());
-        P.n_bnd = static_cast<int64_t>(rows_bnd.size());
-        P.op_int = prepare_rows(rows_int, lro, lci, bv + bro[0], P.nloc + P.nghost, kid, cfg, opts, s);
-        P.op_bnd = prepare_rows(rows_bnd, lro, lci, bv + bro[0], P.nloc + P.nghost, kid, cfg, opts, s);
+        DevBuf<int32_t> rows_int, rows_bnd;
+        P.n_int = flagged_rows(has_ghost, P.nloc, false, rows_int, s);
+        P.n_bnd = flagged_rows(has_ghost, P.nloc, true, rows_bnd, s);
+        has_ghost.release();
+        P.op_int = prepare_rows(*local, rows_int, P.n_int, kid, cfg, opts, s);
+        P.op_bnd = prepare_rows(*local, rows_bnd, P.n_bnd, kid, cfg, opts, s);
     } else {
-        P.local = csr_upload(P.nloc, P.nloc + P.nghost, P.nloc + 1, lro.data(), lnnz, lci.data(), bv + bro[0],
-                             EW_MEM_HOST, false, s);
-        P.op = prepare(kid, *P.local, cfg, opts, s);
+        has_ghost.release();
+        P.op = prepare(kid, *local, cfg, opts, s);
+        // the K1 / K2 layout holds its own copy of the entries; other kernel
+        // kinds keep referring to the local CSR
+        if (kid != "k1" && kid != "k2") P.local = local;
     }
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    local.reset();
     P.send_idx.alloc(sidx.size());
     P.send_buf.alloc(sidx.size());
     if (!sidx.empty())

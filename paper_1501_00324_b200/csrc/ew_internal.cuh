@@ -235,17 +235,28 @@ struct CgWorkspace {
     }
 };
 
-// Host-buffer apply of a large K1 kernel as a copy / compute pipeline: the
-// rows split into B contiguous blocks, each with its own K1 layout (same
-// per-row entry order, so the same row sums); x goes up in B column chunks,
-// block b runs once the chunk holding its largest column has landed, and its
-// y rows go down while later blocks compute (PCIe is full duplex).
+// Host-buffer apply of a large K1 kernel as a copy / compute pipeline over
+// the kernel's own layout (no second copy of the matrix): x goes up in B
+// column chunks; the layout's warps run in B stages, stage b holding every
+// warp whose rows all lie in row blocks <= b (chunk c's columns cover every
+// column the rows of blocks <= c reference, so stage b needs chunks <= b).
+// Row block b goes down after stage ystage[b] (usually b) while later stages
+// compute (PCIe is full duplex); the few rows of a block whose warp runs
+// later than that ("stragglers": e.g. mesh edge rows sharing a warp with rows
+// of every block) are gathered after the last stage and written into y on
+// the host. Same warps, lanes and padding as one whole-layout launch: the
+// same y, bit for bit, for any x.
 struct HostPipeline {
-    int nblocks = 0;
-    std::vector<int64_t> r0;       // row bounds, nblocks + 1
-    std::vector<int64_t> c0;       // x chunk bounds, nblocks + 1
-    std::vector<int> need;         // per block: last x chunk it reads
-    std::vector<std::shared_ptr<LayoutData>> blocks;
+    int nstages = 0;
+    std::vector<int64_t> c0;       // x chunk bounds, nstages + 1
+    std::vector<int64_t> r0;       // row block bounds, nstages + 1
+    std::vector<int> ystage;       // per row block: the stage after which it goes down
+    std::vector<int64_t> wstart;   // stage b runs widx[wstart[b], wstart[b + 1])
+    DevBuf<int32_t> widx;          // layout warps in stage order
+    std::vector<int32_t> late;     // straggler rows (ascending)
+    DevBuf<int32_t> late_d;
+    DevBuf<double> late_y;
+    double* late_h = nullptr;      // pinned
     DevBuf<double> x, y;
     cudaStream_t up = nullptr, down = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
@@ -260,6 +271,7 @@ struct HostPipeline {
         if (ev_done) cudaEventDestroy(ev_done);
         if (up) cudaStreamDestroy(up);
         if (down) cudaStreamDestroy(down);
+        if (late_h) cudaFreeHost(late_h);
     }
 };
 
@@ -274,8 +286,8 @@ struct KernelData {
     DevBuf<int64_t> entry_dst;           // r / rs: original entry -> reordered entry (refresh)
     // CG working sets for cg_solve (0) and cg_solve_permuted (1)
     mutable CgWorkspace cg_ws[2];
-    // host-buffer apply pipeline (built on first use from the layout; dropped
-    // whenever the layout's values change)
+    // host-buffer apply pipeline (built on first use; holds a stage plan of
+    // the layout's warps and staging vectors, no matrix values)
     mutable std::mutex pipe_mu;
     mutable std::unique_ptr<HostPipeline> pipe;
 };
@@ -283,10 +295,6 @@ struct KernelData {
 // y = A x with x, y in host memory through the kernel's HostPipeline; false
 // when the kernel does not qualify (not a large plain K1) or is busy.
 bool kernel_apply_host(const KernelData& k, const double* x, double* y, cudaStream_t s);
-inline void drop_host_pipeline(KernelData& k) {
-    std::lock_guard<std::mutex> g(k.pipe_mu);
-    k.pipe.reset();
-}
 
 std::shared_ptr<FormatData> build_format(const CsrData& m, const std::string& id, int32_t ws, int64_t hyb_k_ell,
                                          cudaStream_t s);
@@ -360,6 +368,10 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
 // done (nullable, device): the launch is a no-op once *done != 0 (CG overrun).
 void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, cudaStream_t s,
                  const int* done = nullptr);
+// Sorted K1, scatter store, over the layout warps widx[0, nidx) only (device
+// list): the host-buffer pipeline runs a layout in stages this way.
+void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, const double* x, double* y,
+                       cudaStream_t s);
 // K1 with x split: columns [0, nown) from x, the rest from xg (scatter store).
 void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,
                        cudaStream_t s);

@@ -1,8 +1,5 @@
 // Prepared kernels: prepare_kernel / apply / apply_permuted (kernels.cpp:14-125)
 // over device layouts.
-#include <cub/device/device_reduce.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include <algorithm>
 #include <cstdlib>
 
@@ -125,96 +122,103 @@ constexpr int64_t kPipeMinNnz = 2'000'000;   // below: one copy each way is chea
 constexpr int64_t kPipeMinRowsPerBlock = 16'384;
 constexpr int kPipeMaxBlocks = 8;
 
-// Row lengths of original rows [r0, r0 + n) from the K1 layout.
-__global__ void block_len_kernel(const int32_t* __restrict__ inv, const int32_t* __restrict__ slen, int64_t r0,
-                                 int64_t n, int64_t* __restrict__ len) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) len[i] = slen[inv[r0 + i]];
+// Largest column of each sorted row position's real entries (-1: no entries).
+__global__ void row_maxcol_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                  const int32_t* __restrict__ slen, int32_t ws_log2, int64_t n,
+                                  int32_t* __restrict__ out) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t ws = int64_t{1} << ws_log2;
+    const int64_t base = woff[p >> ws_log2] + (p & (ws - 1));
+    int32_t m = -1;
+    for (int32_t j = 0; j < slen[p]; ++j) m = max(m, cols[base + j * ws]);
+    out[p] = m;
 }
 
-// The CSR rows [r0, r0 + n) read back out of the K1 slabs (entry order as
-// stored, i.e. the original CSR order), plus the block's largest column.
-__global__ void block_extract_kernel(const double* __restrict__ vals, const int32_t* __restrict__ cols,
-                                     const int64_t* __restrict__ woff, const int32_t* __restrict__ inv,
-                                     int32_t ws_log2, int64_t r0, int64_t n, const int64_t* __restrict__ ro,
-                                     int32_t* __restrict__ ci, double* __restrict__ v, int* cmax) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t p = inv[r0 + i];
-    const int64_t w = p >> ws_log2, ws = int64_t{1} << ws_log2;
-    const int64_t base = woff[w] + (p & (ws - 1));
-    int m = -1;
-    for (int64_t k = ro[i], j = 0; k < ro[i + 1]; ++k, ++j) {
-        const int32_t c = cols[base + j * ws];
-        ci[k] = c;
-        v[k] = vals[base + j * ws];
-        m = max(m, c);
-    }
-    atomicMax(cmax, m);
-}
-
+// The stage plan of HostPipeline (see ew_internal.cuh), from the layout's
+// row permutation and each row's largest column; host work, once per kernel.
 std::unique_ptr<HostPipeline> build_pipeline(const KernelData& k, cudaStream_t s) {
     const LayoutData& l = *k.layout;
-    const int64_t n = k.nrows;
+    const int64_t n = k.nrows, nc = k.ncols, ws = l.ws;
     auto P = std::make_unique<HostPipeline>();
     static const int max_blocks = [] {
         const char* e = std::getenv("EW_PIPE_BLOCKS");  // A/B runs
-        return e ? std::max(1, std::atoi(e)) : kPipeMaxBlocks;
+        return e ? std::min(64, std::max(1, std::atoi(e))) : kPipeMaxBlocks;
     }();
     const int B = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_blocks, n / kPipeMinRowsPerBlock)));
-    P->nblocks = B;
-    P->r0.resize(B + 1);
-    P->c0.resize(B + 1);
-    for (int b = 0; b <= B; ++b) {
-        P->r0[b] = n * b / B;
-        P->c0[b] = k.ncols * b / B;
-    }
-    ew_warp_config cfg{l.ws, std::max(32, l.ws), l.segment_bytes, l.align, 0, 64};
-    DevBuf<int> cmax(B);
-    EW_CUDA_CHECK(cudaMemsetAsync(cmax.get(), 0xff, B * sizeof(int), s));  // -1
-    for (int b = 0; b < B; ++b) {
-        const int64_t nb = P->r0[b + 1] - P->r0[b];
-        CsrData sub;
-        sub.nrows = nb;
-        sub.ncols = k.ncols;
-        sub.ro.alloc(nb + 1);
-        Scratch<int64_t> len(nb, s), mx(1, s);
-        block_len_kernel<<<grid_for(nb), kBlock, 0, s>>>(l.inv.get(), l.slen.get(), P->r0[b], nb, len.get());
-        launched("block_len_kernel");
-        size_t bytes = 0, bytes2 = 0;
-        EW_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, bytes, len.get(), sub.ro.get() + 1, nb, s));
-        EW_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, bytes2, len.get(), mx.get(), nb, s));
-        Scratch<unsigned char> tmp(std::max(bytes, bytes2), s);
-        EW_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, len.get(), sub.ro.get() + 1, nb, s));
-        launched("cub::DeviceScan::InclusiveSum");
-        EW_CUDA_CHECK(cub::DeviceReduce::Max(tmp.get(), bytes2, len.get(), mx.get(), nb, s));
-        launched("cub::DeviceReduce::Max");
-        EW_CUDA_CHECK(cudaMemsetAsync(sub.ro.get(), 0, sizeof(int64_t), s));
-        int64_t nnz = 0, longest = 0;
-        EW_CUDA_CHECK(cudaMemcpyAsync(&nnz, sub.ro.get() + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        EW_CUDA_CHECK(cudaMemcpyAsync(&longest, mx.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    P->nstages = B;
+    std::vector<int32_t> fwd(n), mxc(n);
+    {
+        DevBuf<int32_t> d(n);
+        row_maxcol_kernel<<<grid_for(n), kBlock, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.slen.get(),
+                                                         l.ws_log2, n, d.get());
+        launched("row_maxcol_kernel");
+        EW_CUDA_CHECK(cudaMemcpyAsync(mxc.data(), d.get(), n * 4, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaMemcpyAsync(fwd.data(), l.fwd.get(), n * 4, cudaMemcpyDeviceToHost, s));
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
-        sub.nnz = nnz;
-        sub.ci.alloc(sub.nnz);
-        sub.v.alloc(sub.nnz);
-        block_extract_kernel<<<grid_for(nb), kBlock, 0, s>>>(l.values.get(), l.cols.get(), l.warp_offset.get(),
-                                                             l.inv.get(), l.ws_log2, P->r0[b], nb, sub.ro.get(),
-                                                             sub.ci.get(), sub.v.get(), cmax.get() + b);
-        launched("block_extract_kernel");
-        sub.maxrow = static_cast<int32_t>(longest);
-        P->blocks.push_back(build_layout(sub, EW_LAYOUT_K1, cfg, 0, true, false, s));
     }
-    std::vector<int> hmax(B);
-    EW_CUDA_CHECK(cudaMemcpyAsync(hmax.data(), cmax.get(), B * sizeof(int), cudaMemcpyDeviceToHost, s));
-    EW_CUDA_CHECK(cudaStreamSynchronize(s));
-    P->need.resize(B);
+    // row blocks r0[b] = n b / B; block(r) = the b with r0[b] <= r < r0[b+1]
+    std::vector<int64_t> r0(B + 1);
+    for (int b = 0; b <= B; ++b) r0[b] = n * b / B;
+    std::vector<int32_t> blk(n);
+    for (int b = 0; b < B; ++b)
+        for (int64_t r = r0[b]; r < r0[b + 1]; ++r) blk[r] = b;
+    // x chunk b ends past every column that rows of blocks <= b reference
+    std::vector<int32_t> rowmax(n, -1);
+    for (int64_t p = 0; p < n; ++p) rowmax[fwd[p]] = mxc[p];
+    P->c0.assign(B + 1, 0);
+    int64_t pref = -1;
     for (int b = 0; b < B; ++b) {
-        const int64_t c = std::max(0, hmax[b]);
-        P->need[b] = static_cast<int>(std::upper_bound(P->c0.begin(), P->c0.end(), c) - P->c0.begin()) - 1;
-        P->need[b] = std::min(std::max(P->need[b], 0), B - 1);
+        for (int64_t r = r0[b]; r < r0[b + 1]; ++r) pref = std::max<int64_t>(pref, rowmax[r]);
+        P->c0[b + 1] = std::min(nc, std::max(P->c0[b], std::max(nc * (b + 1) / B, pref + 1)));
     }
-    P->x.alloc(k.ncols);
+    P->c0[B] = nc;
+    // stage of a warp: the last row block it writes (so chunks <= stage cover it)
+    const int64_t nw = l.nwarps;
+    std::vector<int32_t> stage(nw, 0);
+    for (int64_t p = 0; p < n; ++p) stage[p / ws] = std::max(stage[p / ws], blk[fwd[p]]);
+    std::vector<int64_t> cnt(B + 1, 0);
+    for (int64_t w = 0; w < nw; ++w) ++cnt[stage[w] + 1];
+    P->wstart.assign(B + 1, 0);
+    for (int b = 0; b < B; ++b) P->wstart[b + 1] = P->wstart[b] + cnt[b + 1];
+    std::vector<int32_t> order(nw);
+    {
+        std::vector<int64_t> at(P->wstart.begin(), P->wstart.end() - 1);
+        for (int64_t w = 0; w < nw; ++w) order[at[stage[w]]++] = static_cast<int32_t>(w);  // stable
+    }
+    // row block b goes down after the first stage >= b by which all but a
+    // few of its rows are final; the rest are stragglers (gathered at the end)
+    std::vector<int32_t> done_at(n);
+    for (int64_t p = 0; p < n; ++p) done_at[fwd[p]] = stage[p / ws];
+    P->r0 = r0;
+    P->ystage.assign(B, B - 1);
+    for (int b = 0; b < B; ++b) {
+        const int64_t nb = r0[b + 1] - r0[b], allow = std::max<int64_t>(1024, nb / 100);
+        std::vector<int64_t> late_by(B + 1, 0);  // rows of block b final only after stage s
+        for (int64_t r = r0[b]; r < r0[b + 1]; ++r) ++late_by[done_at[r]];
+        int64_t later = nb;
+        for (int st = 0; st < B; ++st) {
+            later -= late_by[st];  // rows final after stage st
+            if (st >= b && later <= allow) {
+                P->ystage[b] = st;
+                break;
+            }
+        }
+        for (int64_t r = r0[b]; r < r0[b + 1]; ++r)
+            if (done_at[r] > P->ystage[b]) P->late.push_back(static_cast<int32_t>(r));
+    }
+    if (!P->late.empty()) {
+        const size_t nl = P->late.size();
+        P->late_d.alloc(nl);
+        P->late_y.alloc(nl);
+        EW_CUDA_CHECK(cudaMallocHost(&P->late_h, nl * sizeof(double)));
+        EW_CUDA_CHECK(cudaMemcpyAsync(P->late_d.get(), P->late.data(), nl * 4, cudaMemcpyHostToDevice, s));
+    }
+    P->widx.alloc(nw);
+    EW_CUDA_CHECK(cudaMemcpyAsync(P->widx.get(), order.data(), nw * 4, cudaMemcpyHostToDevice, s));
+    P->x.alloc(nc);
     P->y.alloc(n);
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
     EW_CUDA_CHECK(cudaStreamCreateWithFlags(&P->up, cudaStreamNonBlocking));
     EW_CUDA_CHECK(cudaStreamCreateWithFlags(&P->down, cudaStreamNonBlocking));
     P->ev_x.resize(B);
@@ -230,7 +234,7 @@ std::unique_ptr<HostPipeline> build_pipeline(const KernelData& k, cudaStream_t s
 
 bool kernel_apply_host(const KernelData& k, const double* x, double* y, cudaStream_t s) {
     if (!k.layout || k.format || k.csr || k.reordered || k.layout->kind != EW_LAYOUT_K1 || k.layout->row_major ||
-        k.layout->imported || k.nnz < kPipeMinNnz || k.nrows < 2 * kPipeMinRowsPerBlock)
+        !k.layout->sorted || k.layout->imported || k.nnz < kPipeMinNnz || k.nrows < 2 * kPipeMinRowsPerBlock)
         return false;
     std::unique_lock<std::mutex> lock(k.pipe_mu, std::try_to_lock);
     if (!lock.owns_lock()) return false;  // a concurrent caller: the plain path
@@ -239,25 +243,48 @@ bool kernel_apply_host(const KernelData& k, const double* x, double* y, cudaStre
     EW_CUDA_CHECK(cudaEventRecord(P.ev_start, s));
     EW_CUDA_CHECK(cudaStreamWaitEvent(P.up, P.ev_start, 0));
     EW_CUDA_CHECK(cudaStreamWaitEvent(P.down, P.ev_start, 0));
-    for (int c = 0; c < P.nblocks; ++c) {
+    for (int c = 0; c < P.nstages; ++c) {
         const int64_t a = P.c0[c], b = P.c0[c + 1];
         if (b > a)
             EW_CUDA_CHECK(cudaMemcpyAsync(P.x.get() + a, x + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice, P.up));
         EW_CUDA_CHECK(cudaEventRecord(P.ev_x[c], P.up));
     }
-    for (int b = 0; b < P.nblocks; ++b) {
-        EW_CUDA_CHECK(cudaStreamWaitEvent(s, P.ev_x[P.need[b]], 0));
-        layout_spmv(*P.blocks[b], P.x.get(), P.y.get() + P.r0[b], /*scatter=*/true, s);
-        EW_CUDA_CHECK(cudaEventRecord(P.ev_y[b], s));
-        EW_CUDA_CHECK(cudaStreamWaitEvent(P.down, P.ev_y[b], 0));
-        const int64_t nb = P.r0[b + 1] - P.r0[b];
-        if (nb)
-            EW_CUDA_CHECK(cudaMemcpyAsync(y + P.r0[b], P.y.get() + P.r0[b], nb * sizeof(double),
-                                          cudaMemcpyDeviceToHost, P.down));
+    for (int b = 0; b < P.nstages; ++b) {
+        EW_CUDA_CHECK(cudaStreamWaitEvent(s, P.ev_x[b], 0));
+        layout_spmv_warps(*k.layout, P.widx.get() + P.wstart[b], P.wstart[b + 1] - P.wstart[b], P.x.get(),
+                          P.y.get(), s);
+        // the row blocks final after this stage (consecutive blocks in one copy)
+        int64_t lo = -1, hi = -1;
+        auto flush = [&] {
+            if (hi > lo)
+                EW_CUDA_CHECK(cudaMemcpyAsync(y + lo, P.y.get() + lo, (hi - lo) * sizeof(double),
+                                              cudaMemcpyDeviceToHost, P.down));
+            lo = hi = -1;
+        };
+        bool recorded = false;
+        for (int rb = 0; rb < P.nstages; ++rb) {
+            if (P.ystage[rb] != b) continue;
+            if (!recorded) {
+                EW_CUDA_CHECK(cudaEventRecord(P.ev_y[b], s));
+                EW_CUDA_CHECK(cudaStreamWaitEvent(P.down, P.ev_y[b], 0));
+                recorded = true;
+            }
+            if (P.r0[rb] != hi) flush();
+            if (lo < 0) lo = P.r0[rb];
+            hi = P.r0[rb + 1];
+        }
+        flush();
+    }
+    const int64_t nl = static_cast<int64_t>(P.late.size());
+    if (nl) {
+        gather(P.late_d.get(), P.y.get(), P.late_y.get(), nl, s);
+        EW_CUDA_CHECK(cudaMemcpyAsync(P.late_h, P.late_y.get(), nl * sizeof(double), cudaMemcpyDeviceToHost, s));
     }
     EW_CUDA_CHECK(cudaEventRecord(P.ev_done, P.down));
     EW_CUDA_CHECK(cudaStreamWaitEvent(s, P.ev_done, 0));
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    // stragglers after their blocks' copies have landed
+    for (int64_t i = 0; i < nl; ++i) y[P.late[i]] = P.late_h[i];
     return true;
 }
 

@@ -21,6 +21,14 @@ namespace ew {
 
 namespace {
 
+// CTA-size A/B knob: a multiple of 32 in [32, 256] (the kernels index one
+// partial per warp and carry __launch_bounds__(256)); anything else -> dflt.
+int cta_size_knob(const char* e, int dflt) {
+    if (!e) return dflt;
+    const int v = std::atoi(e);
+    return (v >= 32 && v <= 256 && v % 32 == 0) ? v : dflt;
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -63,6 +71,8 @@ struct K1Args {
     int32_t nown;
     const uint16_t* cols16;   // COMPACT: 16-bit column offsets (LayoutData::cols16)
     const int32_t* col_base;  // COMPACT: per-warp smallest column
+    const int32_t* widx;      // INDIRECT: the layout warps to run, thread i -> warp widx[i / ws]
+    int64_t nidx;             // INDIRECT: entries of widx
 };
 
 __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p, uint64_t pol) {
@@ -204,10 +214,19 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
 #ifndef EW_K1P_MINB
 #define EW_K1P_MINB 8
 #endif
-template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool COMPACT = false>
+// INDIRECT runs only the layout warps listed in widx (the host-buffer
+// pipeline's stages, ew_kernel.cu): the same warps, lanes and padding as the
+// whole-layout launch, so the same row sums.
+template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool COMPACT = false,
+          bool INDIRECT = false>
 __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_kernel(K1Args a) {
     pdl_wait();
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (INDIRECT) {
+        const int64_t i = p >> a.ws_log2;
+        if (i >= a.nidx) return;
+        p = (int64_t(a.widx[i]) << a.ws_log2) | (p & (a.ws - 1));
+    }
     if (p >= a.nrows || (a.done && *a.done)) return;
     const uint64_t pol = evict_first_policy();
     // the scatter target is loaded with the metadata, not after the row sum
@@ -433,7 +452,7 @@ void launch_k1(const K1Args& a, bool row_major, bool stream_form, bool compact, 
         // 139.6 us, A/B in one box; 128: 139.7-141.6)
         static const int cb = [] {
             const char* e = std::getenv("EW_K1C_BLOCK");  // A/B runs: CTA size of the 16-bit-column K1
-            return e ? std::atoi(e) : 64;
+            return cta_size_knob(e, 64);
         }();
         launch_pdl(k1_kernel<SORTED, SCATTER, false, false, true>, grid_for(a.nrows, cb), cb, s, a);
     }
@@ -492,7 +511,7 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     // partials stay one per warp, in warp order, and no more of them
     static const int cb = [] {
         const char* e = std::getenv("EW_K1C_DOT_BLOCK");  // A/B runs
-        return e ? std::atoi(e) : 64;
+        return cta_size_knob(e, 64);
     }();
     const int block = c ? cb : 256;
     const unsigned g = grid_for(l.nrows, block);
@@ -548,6 +567,21 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     } else {
         scatter ? launch_k2<false, true>(a, s) : launch_k2<false, false>(a, s);
     }
+}
+
+void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, const double* x, double* y,
+                       cudaStream_t s) {
+    require(l.kind == EW_LAYOUT_K1 && !l.row_major && l.sorted, "warp-list SpMV: sorted column-major K1 only");
+    if (nidx == 0 || l.nrows == 0) return;
+    K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
+             l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
+             l.cols16.get(), l.col_base.get(), widx, nidx};
+    const int64_t threads = nidx << l.ws_log2;
+    if (l.compact)
+        launch_pdl(k1_kernel<true, true, false, false, true, true>, grid_for(threads, 64), 64, s, a);
+    else
+        launch_pdl(k1_kernel<true, true, false, false, false, true>, grid_for(threads), kBlock, s, a);
+    launched("k1_kernel");
 }
 
 void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,

@@ -253,9 +253,24 @@ def box_csr_slabbed(kind, nx, ny, nz, nslabs=16, workers=1, **kw):
     columns and values, `workers` slabs at a time on threads): for the
     100M-row config 5 on one GPU, without holding a second copy. Equals
     elasticity_box / laplacian_box."""
+    _, n, ro, ci, v = box_rows_slabbed(kind, nx, ny, nz, 0, nz + 1, nslabs=nslabs, workers=workers, **kw)
+    return n, n, ro, ci, v
+
+
+def box_rows_slabbed(kind, nx, ny, nz, k0=0, k1=None, nslabs=None, workers=8, **kw):
+    """box_rows(kind, nx, ny, nz, k0, k1) built `nslabs` node-layer slabs at a
+    time straight into the final arrays (`workers` slabs concurrently on
+    threads): a partitioned solver's row block of config 5 without the
+    dense per-stencil staging of the whole block. Returns (row_begin,
+    nrows_global, ro, ci, v) with global column ids, equal to box_rows."""
     blk = 1 if kind == "laplacian" else 3
-    n = (nx + 1) * (ny + 1) * (nz + 1) * blk
-    layers = slab_layers(nz, nslabs)
+    k1 = nz + 1 if k1 is None else k1
+    nl = k1 - k0
+    if nslabs is None:
+        nslabs = max(1, nl // 8)
+    nrow_layer = (nx + 1) * (ny + 1) * blk
+    n = nl * nrow_layer
+    layers = [k0 + round(s * nl / nslabs) for s in range(nslabs + 1)]
     ro = np.empty(n + 1, np.int64)
     ro[0] = 0
     start = 0
@@ -267,14 +282,16 @@ def box_csr_slabbed(kind, nx, ny, nz, nslabs=16, workers=1, **kw):
     nnz = int(ro[n])
     ci = np.empty(nnz, np.int64)
     v = np.empty(nnz, np.float64)
+    row0 = k0 * nrow_layer
 
     def fill(slab):
-        k0, k1 = layers[slab], layers[slab + 1]
-        if k1 <= k0:
+        a, b = layers[slab], layers[slab + 1]
+        if b <= a:
             return
-        rb, _, r, c, vv = box_rows(kind, nx, ny, nz, k0, k1, **kw)
-        ci[ro[rb]:ro[rb] + c.size] = c
-        v[ro[rb]:ro[rb] + c.size] = vv
+        rb, _, r, c, vv = box_rows(kind, nx, ny, nz, a, b, **kw)
+        at = ro[rb - row0]
+        ci[at:at + c.size] = c
+        v[at:at + c.size] = vv
 
     if workers <= 1:
         for slab in range(nslabs):
@@ -286,7 +303,7 @@ def box_csr_slabbed(kind, nx, ny, nz, nslabs=16, workers=1, **kw):
 
         with ThreadPoolExecutor(workers) as ex:
             list(ex.map(fill, range(nslabs)))
-    return n, n, ro, ci, v
+    return row0, (nx + 1) * (ny + 1) * (nz + 1) * blk, ro, ci, v
 
 
 def elasticity_box_slabbed(nx=321, ny=321, nz=321):

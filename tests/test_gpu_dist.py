@@ -266,3 +266,32 @@ def test_bench_two_ranks_functional(tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["transport"] == "ipc"
     assert line["cg"]["n_gpus"] == 2 and line["cg"]["value"] > 0
     assert line["cg"]["config"]["final_residual"] < 1.0
+
+
+def test_bench_one_gpu_all_lines():
+    """bench.py at N=1 on scaled-down configs: the SpMV headline plus the
+    config-4 CG line in both row orders and the partitioned config-5 CG
+    line (strong-scaling path with one rank), every timed solve at full
+    length."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--scale", "0.15", "--iterations", "60",
+           "--cg-steps", "2", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0
+    c4 = line["cg_c4"]
+    assert c4["value"] > 0 and c4["config"]["row_order"] == "locality"
+    assert c4["config"]["iterations_run"] == [60, 60]
+    assert c4["reference_row_order"]["value"] > 0
+    c5 = line["cg"]
+    assert c5["scaling"] == "strong" and c5["config"]["config"] == "c5" and c5["value"] > 0
+    assert c5["config"]["iterations_run"] == [60, 60]

@@ -247,9 +247,10 @@ def test_baseline_formats_long_rows_and_stored_slots(ew, F):
 
 def test_host_buffer_pipeline(ew, R, F):
     """ew_kernel_apply with host buffers on a large K1 (>= 2M nnz) runs as a
-    block pipeline (x up in chunks, y down per row block while later blocks
-    compute): bitwise the device apply, also after a values-only refresh
-    (the pipeline's block layouts are rebuilt from the refreshed layout)."""
+    staged pipeline over the kernel's own layout (x up in chunks, the warps
+    in stages, finished y rows down while later stages compute): bitwise the
+    device apply, also after a values-only refresh (the stage plan holds no
+    values)."""
     from oracle.oracle import Csr
     from paper_1501_00324_b200 import workloads as W
 
@@ -276,3 +277,60 @@ def test_host_buffer_pipeline(ew, R, F):
         assert np.array_equal(bits(k.apply(x)), bits(R.spmv_layout(lay, x, scatter=True)))
     finally:
         R.free(lay)
+
+
+def _nan_eq(a, b):
+    """Bitwise, except that any NaN equals any NaN (payloads are not part of
+    the reference's semantics)."""
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and np.array_equal(bits(a)[~na], bits(b)[~nb])
+
+
+@pytest.mark.parametrize("shape", ["mesh", "random_graph"])
+def test_host_buffer_pipeline_nonfinite_x0(ew, R, F, shape):
+    """The reference K1 adds 0.0 * x[0] for every padding slot of a lane
+    (warp_spmv.cpp:30-34), so a non-finite x[0] turns exactly the padded rows
+    (and the rows that read column 0) into NaN. The host-buffer pipeline runs
+    the kernel's own warps, so its y matches the reference K1 for any x:
+    NaN / +-Inf at x[0], and signed zeros, on >= 2M nnz (a mesh in natural
+    order, staged, and a random graph whose rows reach across all of x)."""
+    import torch
+
+    from oracle.oracle import Csr
+    from paper_1501_00324_b200 import workloads as W
+
+    if shape == "mesh":
+        n, _, ro, ci, v = W.elasticity_box(30, 30, 30)
+        m = Csr.make(n, n, ro, ci, v)
+    else:
+        m = F.fem_tet_graph(100_000, 8, 40, 7)
+    assert m.nnz >= 2_000_000
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    lay = R.build_k1(m)
+    padded_rows = 0
+    try:
+        lens = np.diff(m.row_offsets)
+        row_pad = np.repeat(lay.maxrows, 32)[: m.nrows] - lay.sorted_row_length
+        padded_rows = int(np.count_nonzero(row_pad > 0))
+        rng = np.random.default_rng(11)
+        for x0 in (np.nan, np.inf, -np.inf, -0.0, 0.0):
+            x = rng.uniform(-1.0, 1.0, m.ncols)
+            x[1::7] = -0.0
+            x[0] = x0
+            want = R.spmv_layout(lay, x, scatter=True)
+            yh = k.apply(x)
+            yd = k.apply(torch.tensor(x, device="cuda")).cpu().numpy()
+            assert _nan_eq(yh, want), x0
+            assert _nan_eq(yd, want), x0
+            if np.isnan(x0) or np.isinf(x0):
+                # padded rows with no column-0 entry are NaN only through padding
+                touches0 = np.zeros(m.nrows, bool)
+                touches0[np.repeat(np.arange(m.nrows), lens)[m.col_indices == 0]] = True
+                pad_only = np.zeros(m.nrows, bool)
+                pad_only[lay.forward[row_pad > 0]] = True
+                pad_only &= ~touches0
+                assert pad_only.any() and np.isnan(yh[pad_only]).all()
+    finally:
+        R.free(lay)
+    assert padded_rows > 0

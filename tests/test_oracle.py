@@ -130,3 +130,42 @@ def test_restatement_cg_error_paths(R, F):
     with pytest.raises(OracleError) as e:
         R.cg_csr(eye, np.ones(8), jacobi=False)
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("kernel,threads", [("k1rs", 4), ("k1", 3), ("k2", 5)])
+def test_threaded_cg_matches_reference(R, F, kernel, threads):
+    """The multi-threaded restatement (SpMV warps and vector updates on host
+    threads, dot products sequential) that the full-size config-4 parity test
+    uses as its checker: bitwise the compiled reference's cg_solve /
+    cg_solve_permuted through prepare_kernel(kernel), history and solution,
+    on a randomly renumbered jittered-mesh operator (config 4's structure at
+    a CPU-test size), 300 forced iterations."""
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.ventricle_box(14, 14, 14)
+    m = Csr.make(n, n, ro, ci, v)
+    b = R.spmv_csr(m, np.ones(n))
+    diag = R.extract_diagonal(m)
+    permuted = kernel.endswith("rs")
+    if permuted:
+        op, _ = R.reorder(m, True)
+        lay = R.build_k1(op)
+    elif kernel == "k2":
+        lay = R.build_k2(m, 4)
+    else:
+        lay = R.build_k1(m)
+    try:
+        x = np.random.default_rng(5).uniform(-1, 1, n)
+        want_y = R.spmv_layout(lay, x, scatter=not permuted)
+        assert np.array_equal(bits(R.spmv_layout(lay, x, scatter=not permuted, threads=threads)), bits(want_y))
+        got = R.cg_layout(lay, b, diag=diag, permuted=permuted, tol=1e-300, max_iterations=300,
+                          threads=threads)
+        one = R.cg_layout(lay, b, diag=diag, permuted=permuted, tol=1e-300, max_iterations=300)
+    finally:
+        R.free(lay)
+    ref = F.cg(kernel, m, b, tol=1e-300, max_iterations=300, permuted=permuted, threshold=4)
+    assert got.iterations == ref.iterations == 300
+    assert got.spmv_calls == ref.spmv_calls == 1 + 300 + 300 // 50
+    for r in (got, one):
+        assert np.array_equal(bits(r.residual_history), bits(ref.residual_history))
+        assert np.array_equal(bits(r.solution), bits(ref.solution))
