@@ -823,34 +823,13 @@ def run_cg(args, rank, world, local):
     return out
 
 
-# The paper's 15-matrix suite (Table 2) as the reference's
-# synthetic stand-ins (bench/fetch.cpp:16-46: generator kind and parameters),
-# scaled to the Table 2 row counts.
-SUITE = [
-    ("circuit", 170998, "powerlaw_rows", dict(alpha=1.4, maxrow=353, seed=11)),
-    ("economics", 206500, "powerlaw_rows", dict(alpha=0.8, maxrow=44, seed=12)),
-    ("epidemiology", 525825, "uniform_band", dict(row_len=4)),
-    ("accelerator", 121192, "fem_tet_graph", dict(minrow=8, maxrow=81, seed=13)),
-    ("cantilever", 62451, "fem_tet_graph", dict(minrow=2, maxrow=78, seed=14)),
-    ("harbor", 46835, "fem_tet_graph", dict(minrow=4, maxrow=145, seed=15)),
-    ("ship", 140874, "fem_tet_graph", dict(minrow=24, maxrow=102, seed=16)),
-    ("spheres", 83334, "fem_tet_graph", dict(minrow=2, maxrow=81, seed=17)),
-    ("protein", 36417, "fem_tet_graph", dict(minrow=18, maxrow=204, seed=18)),
-    ("qcd", 49152, "uniform_band", dict(row_len=39)),
-    ("webbase", 1000005, "powerlaw_rows", dict(alpha=2.0, maxrow=1000, seed=19)),
-    ("windtunnel", 217918, "fem_tet_graph", dict(minrow=2, maxrow=180, seed=20)),
-    ("heart3k", 3129, "fem_tet_graph", dict(minrow=5, maxrow=21, seed=3)),
-    ("heart5k", 4563, "fem_tet_graph", dict(minrow=6, maxrow=22, seed=5)),
-    ("heart30k", 28639, "fem_tet_graph", dict(minrow=6, maxrow=24, seed=30)),
-]
+# Config 3: the paper's 15-matrix suite (Table 2) at its
+# Table 2 sizes: seeded stand-ins whose nz / nrows / minrow / maxrow are
+# Table 2's (workloads.TABLE2, table2_matrix; tests/test_workloads.py).
+def suite_names():
+    from paper_1501_00324_b200 import workloads as W
 
-
-def suite_matrix(ew_mod, kind, n, p):
-    if kind == "powerlaw_rows":
-        return ew_mod.powerlaw_rows(n, p["alpha"], p["maxrow"], p["seed"])
-    if kind == "uniform_band":
-        return ew_mod.uniform_band(n, p["row_len"])
-    return ew_mod.fem_tet_graph(n, p["minrow"], p["maxrow"], p["seed"])
+    return [t[0] for t in W.TABLE2]
 
 
 def run_suite(args):
@@ -868,16 +847,27 @@ def run_suite(args):
     kernels = ["k1", "k1rs", "k2", "csr_ref", "csr_vector", "ell", "hyb", "coo", "k1rs_loc", "k2rs_loc"]
     rows = []
     stream = torch.cuda.current_stream()
-    for name, n, kind, p in SUITE:
+    from paper_1501_00324_b200 import workloads as W
+
+    table = {t[0]: t for t in W.TABLE2}
+    only = set(args.suite_only.split(",")) if args.suite_only else None
+    for name in suite_names():
+        if only and name not in only:
+            continue
         t = time.time()
-        m = suite_matrix(ew_mod, kind, n, p)
-        ro = np.asarray(m.row_offsets, np.int64)
+        mn, mc, ro, ci, v = W.table2_matrix(name, ew_mod)
         lens = np.diff(ro)
-        a = capi.Csr(m.nrows, m.ncols, ro, np.asarray(m.col_indices, np.int64), np.asarray(m.values))
+        a = capi.Csr(mn, mc, ro, ci, v)
         nnz = a.nnz
+        m = argparse.Namespace(nrows=mn, ncols=mc)
         x = torch.tensor(np.random.default_rng(1).uniform(0.1, 1.0, m.ncols), device="cuda")
         y = torch.empty(m.nrows, dtype=torch.float64, device="cuda")
+        kind, spec = W.table2_spec(name)
+        _, t_nnz, t_rows, t_min, t_max = table[name]
         rec = {"matrix": name, "nrows": m.nrows, "nnz": nnz, "minrow": int(lens.min()), "maxrow": int(lens.max()),
+               "table2": {"nz": t_nnz, "nrows": t_rows, "minrow": t_min, "maxrow": t_max},
+               "generator": {"kind": kind, **{k2: (round(v2, 6) if isinstance(v2, float) else v2)
+                                              for k2, v2 in spec.items()}},
                "gen_s": round(time.time() - t, 1)}
         for kid in kernels:
             thresholds = [0] if not kid.startswith("k2") else sorted({4, 8, 16, 32, max(1, int(lens.max()))})
@@ -935,7 +925,8 @@ def run_suite(args):
                                  key=lambda kk: r[kk]["eff_gbs"]) for r in rows}
     return {"metric": "SpMV effective GB/s per matrix (20 B/nnz), L2 flushed (evict_last read of 256 MB) before each launch; "
                       "warm_*: back-to-back launches",
-            "workload": "config 3: 15 synthetic structures at Table 2 sizes (bench/fetch.cpp stand-ins)",
+            "workload": "config 3: 15 seeded stand-ins with Table 2's nz / nrows / minrow / maxrow "
+                        "(workloads.TABLE2; generator kinds of bench/fetch.cpp)",
             "unit": "GB/s", "peak": hbm, "peak_source": peak_src, "iterations": args.suite_iters,
             "fastest_kernel": best_k,
             "fastest_including_locality_order": best_all,
@@ -979,11 +970,13 @@ def run_alpha(args):
             ts.append(time.perf_counter() - t)
         return float(np.median(ts))
 
+    from paper_1501_00324_b200 import workloads as W
+
     rows = []
-    for name, n, kind, p in SUITE:
-        m = suite_matrix(ew_mod, kind, n, p)
-        ro = np.asarray(m.row_offsets, np.int64)
-        a = capi.Csr(m.nrows, m.ncols, ro, np.asarray(m.col_indices, np.int64), np.asarray(m.values))
+    for name in suite_names():
+        mn, mc, ro, ci, v = W.table2_matrix(name, ew_mod)
+        a = capi.Csr(mn, mc, ro, ci, v)
+        m = argparse.Namespace(nrows=mn, ncols=mc)
         x = torch.tensor(np.random.default_rng(1).uniform(0.1, 1.0, m.ncols), device="cuda")
         y = torch.empty(m.nrows, dtype=torch.float64, device="cuda")
         base = capi.Kernel("csr_ref", a)
@@ -1049,6 +1042,7 @@ def main():
     p.add_argument("--workload", choices=["spmv", "cg", "suite", "alpha"], default="spmv")
     p.add_argument("--alpha-reps", type=int, default=9)
     p.add_argument("--suite-iters", type=int, default=5)
+    p.add_argument("--suite-only", default="", help="comma-separated Table 2 names (suite workload)")
     p.add_argument("--config", default=None)
     p.add_argument("--kernel", default=None)
     p.add_argument("--threshold", type=int, default=0)
