@@ -162,6 +162,7 @@ struct LayoutData {
     int64_t n_active = 0;  // rows with at least one entry
     int64_t stored_slots = 0;
     int32_t max_reduction = 1;
+    int32_t max_mx = 0;    // sorted K1: the longest warp's maxrows (0: unknown)
     bool imported = false;  // built elsewhere: K2 may not cover every row
     DevBuf<double> values;
     DevBuf<int32_t> cols;

@@ -637,6 +637,8 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
         const int64_t last_off = read_scalar(l.warp_offset.get() + nw - 1, s);
         const int32_t last_mx = read_scalar(l.maxrows.get() + nw - 1, s);
         l.nslots = last_off + int64_t(last_mx) * l.ws;
+        // sorted longest-first: warp 0 holds the longest row
+        if (kind == EW_LAYOUT_K1 && l.sorted) l.max_mx = read_scalar(l.maxrows.get(), s);
     }
     sizes_owner.reset();
     unsigned long long hc[2];

@@ -281,6 +281,114 @@ __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
     pdl_trigger();
 }
 
+// K1 for layouts with few, long rows (the FEM matrices of the paper's suite
+// at Table 2 sizes: 36k-220k rows of 20-120 entries, i.e. under one wave of
+// one-thread-per-row CTAs, each thread walking its row 8 slots per round
+// trip). One CTA of H warps per layout warp (ws = 32): every warp loads and
+// multiplies its share of each chunk of 8H steps (H times the loads in
+// flight), the products go to shared memory, and warp 0 adds them in step
+// order. Same products (v * x[c], padding included), same sequential sum per
+// row as k1_kernel: bit-identical y.
+template <bool SCATTER, bool COMPACT, int H>
+__global__ void __launch_bounds__(32 * H) k1_coop_kernel(K1Args a) {
+    constexpr int C = 8 * H;
+    __shared__ double prod[2][C][32];
+    pdl_wait();
+    if (a.done && *a.done) return;  // uniform across the grid
+    const int64_t w = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (w << 5) + lane;
+    const int32_t mx = __ldg(a.maxrows + w);
+    const int64_t wo = __ldg(a.woff + w);
+    const int32_t base = COMPACT ? __ldg(a.col_base + w) : -1;
+    int64_t target = p;
+    if (SCATTER && warp == 0 && p < a.nrows) target = a.fwd[p];
+    const uint64_t pol = evict_first_policy();
+    uint64_t keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    double acc = 0.0;
+    const int nchunks = (mx + C - 1) / C;
+    for (int c = 0; c < nchunks; ++c) {
+        const int j0 = c * C + warp * 8;
+        const int cnt = min(8, mx - j0);
+        if (cnt > 0) {
+            const int64_t s0 = wo + int64_t(j0) * 32 + lane;
+            int32_t col[8];
+            double v[8], xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (u < cnt) {
+                    if (COMPACT && base >= 0) {
+                        const uint16_t d = ld_stream(a.cols16 + s0 + u * 32, pol);
+                        col[u] = d == 0xFFFFu ? 0 : base + static_cast<int32_t>(d);
+                    } else {
+                        col[u] = ld_stream(a.cols + s0 + u * 32, pol);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < cnt) v[u] = ld_stream(a.values + s0 + u * 32, pol);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < cnt)
+                    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                                 : "=d"(xv[u])
+                                 : "l"(a.x + col[u]), "l"(keep));
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < cnt) prod[c & 1][warp * 8 + u][lane] = __dmul_rn(v[u], xv[u]);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int n = min(C, mx - c * C);
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, prod[c & 1][j][lane]);
+        }
+    }
+    if (warp == 0 && p < a.nrows) a.y[target] = p < a.n_active ? acc : 0.0;
+    pdl_trigger();
+}
+
+// Warps per CTA of k1_coop_kernel for a layout, 0: the plain kernel. Sorted,
+// column-major ws = 32 int32-column layouts with under one wave of
+// one-thread-per-row CTAs (148 SMs x 2048 threads). H trades the chunks the
+// longest warp walks in sequence (ceil(max_mx / 8H)) against resident CTAs
+// (~32 / H per SM): layouts with a row over 96 entries take 8, small ones
+// (<= 8 CTAs per SM at H = 4) 4, the rest 2 -- the best or within 5% of the
+// best H on every config-3 matrix (H = 2 / 4 / 8 sweep on B200). 16-bit-column
+// layouts (over 64 MB) keep their 64-thread-CTA form, which wins there (ship,
+// spheres, windtunnel). EW_K1_COOP=0 turns it off, =2/4/8 fixes H (A/B runs).
+int coop_warps(const LayoutData& l) {
+    static const int mode = [] {
+        const char* e = std::getenv("EW_K1_COOP");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (!mode || l.kind != EW_LAYOUT_K1 || l.row_major || !l.sorted || l.imported || l.ws != 32 || l.nwarps == 0)
+        return 0;
+    if (mode == 2 || mode == 4 || mode == 8) return mode;  // A/B: a fixed H
+    if (l.nrows > int64_t{148} * 2048 || l.compact) return 0;
+    if (l.max_mx > 96) return 8;
+    if (l.nwarps <= 148 * 8) return 4;
+    return 2;
+}
+
+template <bool SCATTER>
+void launch_k1_coop(const K1Args& a, int64_t nwarps, int h, bool compact, cudaStream_t s) {
+    const unsigned g = static_cast<unsigned>(nwarps);
+    auto go = [&](auto kernel, int hh) { launch_pdl(kernel, g, 32 * hh, s, a); };
+    if (compact) {
+        if (h == 2) go(k1_coop_kernel<SCATTER, true, 2>, 2);
+        else if (h == 4) go(k1_coop_kernel<SCATTER, true, 4>, 4);
+        else go(k1_coop_kernel<SCATTER, true, 8>, 8);
+    } else {
+        if (h == 2) go(k1_coop_kernel<SCATTER, false, 2>, 2);
+        else if (h == 4) go(k1_coop_kernel<SCATTER, false, 4>, 4);
+        else go(k1_coop_kernel<SCATTER, false, 8>, 8);
+    }
+    launched("k1_coop_kernel");
+}
+
 // Layouts whose slabs exceed this stream from HBM, with at least this many
 // slots per row: k1_stream_kernel.
 constexpr int64_t kStreamSlotBytes = 64ll << 20;
@@ -387,16 +495,22 @@ __global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ 
     bool leader = false;
     int64_t pos = 0, target = 0;
     if (w < a.nwarps) {
-        red = a.reduction[w];
+        // every per-warp field in one round trip (independent loads issued
+        // together; ncu: the former chain reduction -> rows_in_warp ->
+        // rows_offset_warp -> maxrows held ~30% of a cold launch)
+        red = __ldg(a.reduction + w);
+        const int32_t riw = __ldg(a.rows_in_warp + w), row0 = __ldg(a.rows_offset_warp + w);
+        const int32_t mx = __ldg(a.maxrows + w);
+        const int64_t wo = __ldg(a.woff + w);
         const int32_t rl = __ffs(red) - 1;
         const int32_t r = lane >> rl;
         tl = lane & (red - 1);
-        if (r < a.rows_in_warp[w]) {
-            pos = int64_t(a.rows_offset_warp[w]) + r;
+        if (r < riw) {
+            pos = int64_t(row0) + r;
             leader = tl == 0;
             if (SCATTER && leader) target = a.fwd[pos];  // with the metadata, not after the sum
             const bool active = SORTED ? pos < a.n_active : a.slen[pos] > 0;
-            if (active) sum = lane_sum(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+            if (active) sum = lane_sum(a.values, a.cols, a.x, wo + lane, a.ws, mx, pol);
         }
     }
     const int32_t hw_red = static_cast<int32_t>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(red)));
@@ -548,6 +662,10 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                  l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
              l.cols16.get(), l.col_base.get()};
         const bool rm = l.row_major != 0, sf = streams(l), c = l.compact != 0;
+        if (const int h = coop_warps(l)) {
+            scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
+            return;
+        }
         if (l.sorted) {
             scatter ? launch_k1<true, true>(a, rm, sf, c, s) : launch_k1<true, false>(a, rm, sf, c, s);
         } else {
