@@ -1,5 +1,6 @@
 // ELL / HYB layouts for padding comparisons (formats.cpp:7-62 in the
-// reference). Their SpMV kernels are SURVEY.md §8(f) "next".
+// reference), host side; their SpMV kernels run on the device
+// (csrc/ew_formats.cu, prepare_kernel("ell" / "hyb")).
 #include "ellwarp/formats.hpp"
 
 namespace ellwarp {

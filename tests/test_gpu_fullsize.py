@@ -125,3 +125,62 @@ def test_config2_partitioned_spmv_bitwise(ew, c2, transport):
     y = d.spmv(x)
     both_zero = (y == 0) & (single == 0)
     assert np.all(both_zero | (bits(y) == bits(single)))
+
+
+def _first_cross(h, ref, thr):
+    n = min(len(h), len(ref))
+    d = np.abs(h[:n] - ref[:n]) / (1.0 + ref[:n])
+    i = np.flatnonzero(d > thr)
+    return int(i[0]) if i.size else n
+
+
+@pytest.mark.parametrize("transport", ["peer", "copy"])
+def test_config5_scaled_partitioned_cg_vs_oracle(ew, R, transport):
+    """The partitioned PCG (4 row blocks, the multi-GPU code path with the
+    in-process peer transport or device copies) on config 5's operator at a
+    test size (3-DOF elasticity box(40,40,40), 206,763 rows), 400 forced
+    iterations, against the restated reference: cg_solve over the K1 layout
+    of the whole matrix (threaded restatement, bitwise the reference). The
+    partitions' dot products are summed in rank order (a different order
+    than the reference's sequential sums), so the history is held to the
+    bar the reference meets against itself with a different summation
+    order: its own cg_solve_permuted over k1rs vs cg_solve over K1
+    (test_solver.cpp:83-112), which itself leaves the comparator
+    |dh| <= 1e-10 (1 + h) at iteration ~219 (CG amplifies rounding
+    differences: the device K1 solve, the 2- and 4-way partitions and the
+    device k1rs solve all leave it at 193-201). Held: the comparator over
+    the first 3/4 of the pair's in-comparator span, every deviation
+    threshold reached no earlier than 3/4 of where the pair reaches it,
+    1 + it + it/50 SpMVs, solution within 1e-9."""
+    import os
+
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.elasticity_box(40, 40, 40)
+    m = Csr.make(n, n, ro, ci, v)
+    b = R.spmv_csr(m, np.ones(n))
+    diag = R.extract_diagonal(m)
+    lay = R.build_k1(m)
+    th = os.cpu_count() or 1
+    try:
+        ref = R.cg_layout(lay, b, diag=diag, tol=1e-300, max_iterations=400, threads=th)
+    finally:
+        R.free(lay)
+    op, _ = R.reorder(m, True)
+    lay = R.build_k1(op)
+    try:
+        perm = R.cg_layout(lay, b, diag=diag, permuted=True, tol=1e-300, max_iterations=400, threads=th)
+    finally:
+        R.free(lay)
+    d = ew.Dist.local(m, 4, transport=transport)
+    res = d.cg_solve(b, diag, tol=1e-300, max_iterations=400)
+    assert res.iterations == 400 and res.spmv_calls == 1 + 400 + 8
+    h, hk, hp = res.residual_history, ref.residual_history, perm.residual_history
+    dev = np.abs(h - hk) / (1.0 + hk)
+    own_dev = np.abs(hp - hk) / (1.0 + hk)
+    msg = f"max deviation {dev.max():.2e} (reference's own k1rs-vs-K1: {own_dev.max():.2e})"
+    own = int(0.75 * _first_cross(hp, hk, 1e-10))
+    assert np.all(dev[:own] <= 1e-10), msg
+    for thr in (1e-10, 1e-8, 1e-6):
+        assert _first_cross(h, hk, thr) >= 0.75 * _first_cross(hp, hk, thr), (thr, msg)
+    assert np.max(np.abs(res.solution - ref.solution)) <= 1e-9 * max(1.0, np.abs(ref.solution).max())

@@ -169,3 +169,38 @@ def test_threaded_cg_matches_reference(R, F, kernel, threads):
     for r in (got, one):
         assert np.array_equal(bits(r.residual_history), bits(ref.residual_history))
         assert np.array_equal(bits(r.solution), bits(ref.solution))
+
+
+def test_config4_fixture_consistent_and_restatement_prefix(R):
+    """The config-4 CG fixtures (tests/golden/make_c4_cg.py, the reference run
+    to tol 1e-8) are self-consistent, and the threaded C restatement
+    reproduces the reference's k1rs history bit for bit over its first 12
+    iterations on the full 5M-row matrix (the whole 2,430 iterations were
+    checked the same way when the fixture was made: --impl restatement)."""
+    import hashlib
+    import os
+
+    from paper_1501_00324_b200 import workloads as W
+
+    golden = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    f = {k: np.load(os.path.join(golden, f"c4_cg_{k}.npz")) for k in ("k1rs", "csr_ref")}
+    for k, fx in f.items():
+        it = int(fx["iterations"])
+        assert bool(fx["converged"]) and fx["history"].size == it + 1
+        assert int(fx["spmv_calls"]) == 1 + it + it // 50
+        assert fx["history"][-1] <= 1e-8 < fx["history"][-2]
+    n, _, ro, ci, v = W.ventricle_box(170, 170, 170)
+    m = Csr.make(n, n, ro, ci, v)
+    h = hashlib.sha256()
+    for a in (m.row_offsets, m.col_indices, m.values):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(f["k1rs"]["matrix_sha256"])
+    b = R.spmv_csr(m, np.ones(n))
+    op, _ = R.reorder(m, True)
+    lay = R.build_k1(op)
+    try:
+        res = R.cg_layout(lay, b, diag=R.extract_diagonal(m), permuted=True, tol=1e-300, max_iterations=12,
+                          threads=os.cpu_count() or 1)
+    finally:
+        R.free(lay)
+    assert np.array_equal(bits(res.residual_history), bits(f["k1rs"]["history"][:13]))
