@@ -355,6 +355,29 @@ ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, v
 ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const ew_cg_config* cfg,
                            ew_mem_kind mem, double* x, double* history, ew_cg_result* result,
                            void* stream);
+/* ---- one process, several GPUs (SURVEY.md §8(b) ew_mgpu_cg_solve) ---------
+ * The square host CSR (validate_csr ranges) split into ngpus nnz-balanced
+ * row blocks (ew_partition_rows); block g lives on device devices[g]
+ * (NULL: device g; a device may repeat, e.g. every block on device 0 for
+ * tests: then set CUDA_DEVICE_MAX_CONNECTIONS >= 2 per block on the device
+ * before the first CUDA call, the blocks' streams wait on each other and
+ * need a hardware queue each). Peers are reached by peer access (NVLink stores) with the same
+ * push / mailbox / rank-ordered reduction kernels as the CUDA-IPC
+ * transport, one host thread and stream per block. Replaces running
+ * ew_dist_create_block_ipc on ngpus processes for callers that are one
+ * process (the reference's CLI `cg`, tools/ellwarp_cli.cpp:186-213; FEM time
+ * stepping, fem/timestep.cpp:90-107). */
+typedef struct ew_mgpu_t* ew_mgpu;
+ew_status ew_mgpu_create(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
+                         int32_t ngpus, const int32_t* devices, const char* kernel_id, const ew_warp_config* cfg,
+                         const ew_kernel_options* opts, ew_mgpu* out);
+ew_status ew_mgpu_destroy(ew_mgpu m);
+/* y = A x; x, y host arrays of nrows. */
+ew_status ew_mgpu_spmv(ew_mgpu m, const double* x, double* y);
+/* cg_solve (cg.cpp:25-104) over the blocks; b, diag, x host arrays of nrows,
+ * history max_iterations + 1 entries (may be NULL). */
+ew_status ew_mgpu_cg_solve(ew_mgpu m, const double* b, const double* diag, const ew_cg_config* cfg, double* x,
+                           double* history, ew_cg_result* result);
 /* ---- FEM assembly as K1 row sums (fem/assembly.cpp:38-159, SURVEY.md
  * §8(f) #3) ---------------------------------------------------------------
  * build_assembly_map on the device: the node-adjacency pattern of the

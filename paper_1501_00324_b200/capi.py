@@ -176,6 +176,11 @@ _SIGS = {
     "ew_dist_spmv": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "ew_dist_cg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(CgConfig), C.c_int, _vp, _vp, C.POINTER(CgResultC),
                                    _vp]),
+    "ew_mgpu_create": (C.c_int, [C.c_int64, _vp, _vp, _vp, C.c_int32, _vp, C.c_char_p, C.POINTER(WarpConfig),
+                                 C.POINTER(KernelOptions), C.POINTER(_vp)]),
+    "ew_mgpu_destroy": (C.c_int, [_vp]),
+    "ew_mgpu_spmv": (C.c_int, [_vp, _vp, _vp]),
+    "ew_mgpu_cg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(CgConfig), _vp, _vp, C.POINTER(CgResultC)]),
 }
 
 _lib = None
@@ -822,3 +827,47 @@ def compute_alpha(t_reorder, t_kernel, t_base):
     f = C.c_int32()
     check(lib().ew_compute_alpha(float(t_reorder), float(t_kernel), float(t_base), C.byref(a), C.byref(f)))
     return a.value if f.value else None
+
+
+class Mgpu:
+    """One process, several GPUs (ew_mgpu_*): the square host CSR in
+    nnz-balanced row blocks, block g on devices[g] (default: device g; a
+    device may repeat), peers over peer access, one host thread per block."""
+
+    def __init__(self, m, ngpus, devices=None, kernel="k1", warp_size=32, threshold=0):
+        ro, ci, v = _host(m.row_offsets, np.int64), _host(m.col_indices, np.int64), _host(m.values, np.float64)
+        dev = _host(devices, np.int32) if devices is not None else None
+        if dev is not None and dev.size != ngpus:
+            raise ValueError("devices must list one device per partition")
+        cfg = WarpConfig.make(warp_size)
+        opts = KernelOptions(int(threshold), -1, 0)
+        h = C.c_void_p()
+        check(lib().ew_mgpu_create(int(m.nrows), _ptr(ro), _ptr(ci), _ptr(v), int(ngpus), _ptr(dev),
+                                   kernel.encode(), C.byref(cfg), C.byref(opts), C.byref(h)))
+        self.h, self.n = h, int(m.nrows)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib is not None:
+            _lib.ew_mgpu_destroy(h)
+            self.h = None
+
+    def spmv(self, x):
+        x = _host(x, np.float64)
+        y = np.empty(self.n, np.float64)
+        check(lib().ew_mgpu_spmv(self.h, _ptr(x), _ptr(y)))
+        return y
+
+    def cg_solve(self, b, diag=None, tol=1e-8, max_iterations=1000, jacobi=True, recompute_interval=50,
+                 divergence_limit=1e6):
+        cfg = CgConfig(float(tol), int(max_iterations), 1 if jacobi else 0, int(recompute_interval),
+                       float(divergence_limit))
+        b = _host(b, np.float64)
+        diag = _host(diag, np.float64) if diag is not None else None
+        x = np.empty(self.n, np.float64)
+        hist = np.empty(int(max_iterations) + 1, np.float64)
+        res = CgResultC()
+        check(lib().ew_mgpu_cg_solve(self.h, _ptr(b), _ptr(diag), C.byref(cfg), _ptr(x), _ptr(hist),
+                                     C.byref(res)))
+        return CgResult(x, int(res.iterations), hist[: res.history_len].copy(), bool(res.converged),
+                        int(res.spmv_calls))

@@ -21,6 +21,9 @@ struct ew_dist_t {
 struct ew_assembly_t {
     std::shared_ptr<ew::AssemblyData> d;
 };
+struct ew_mgpu_t {
+    std::shared_ptr<ew::MgpuData> d;
+};
 
 namespace {
 
@@ -780,6 +783,48 @@ ew_status ew_dist_cg_solve(ew_dist d, const double* b, const double* diag, const
         ew::CgOutputs o = ew::dist_cg(*d->d, bp, jac ? dp : nullptr, *cfg, xp, s);
         if (mem == EW_MEM_HOST && n) EW_CUDA_CHECK(cudaMemcpyAsync(x, xd.get(), n * 8, cudaMemcpyDeviceToHost, s));
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        *result = o.res;
+        if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+    });
+}
+
+ew_status ew_mgpu_create(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
+                         int32_t ngpus, const int32_t* devices, const char* kernel_id, const ew_warp_config* cfg,
+                         const ew_kernel_options* opts, ew_mgpu* out) {
+    return guarded([&] {
+        ew::require(out != nullptr && row_offsets != nullptr && kernel_id != nullptr, "null argument");
+        ew::require(nrows >= 0 && row_offsets[0] == 0, "row_offsets[0] != 0");
+        if (nrows > 0x7fffffff) throw ew::Error(EW_UNSUPPORTED, "device path supports at most 2^31-1 rows");
+        const int64_t nnz = row_offsets[nrows];
+        ew::require(nnz == 0 || (col_indices != nullptr && values != nullptr), "col_indices/values are null");
+        for (int64_t r = 0; r < nrows; ++r)
+            ew::require(row_offsets[r] <= row_offsets[r + 1], "row_offsets not nondecreasing");
+        for (int64_t k = 0; k < nnz; ++k)
+            ew::require(col_indices[k] >= 0 && col_indices[k] < nrows, "column out of range");
+        const ew_warp_config c = cfg ? *cfg : default_config();
+        const ew_kernel_options o = opts ? *opts : ew_kernel_options{0, -1};
+        *out = new ew_mgpu_t{ew::mgpu_create(nrows, row_offsets, col_indices, values, ngpus, devices, kernel_id, c, o)};
+    });
+}
+
+ew_status ew_mgpu_destroy(ew_mgpu m) {
+    return guarded([&] { delete m; });
+}
+
+ew_status ew_mgpu_spmv(ew_mgpu m, const double* x, double* y) {
+    return guarded([&] {
+        check_handle(m, "mgpu");
+        ew::require(x != nullptr && y != nullptr, "null argument");
+        ew::mgpu_spmv(*m->d, x, y);
+    });
+}
+
+ew_status ew_mgpu_cg_solve(ew_mgpu m, const double* b, const double* diag, const ew_cg_config* cfg, double* x,
+                           double* history, ew_cg_result* result) {
+    return guarded([&] {
+        check_handle(m, "mgpu");
+        ew::require(cfg != nullptr && result != nullptr && b != nullptr && x != nullptr, "null argument");
+        ew::CgOutputs o = ew::mgpu_cg(*m->d, b, diag, *cfg, x);
         *result = o.res;
         if (history) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
     });

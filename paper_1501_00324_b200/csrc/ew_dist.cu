@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "ew_cg.cuh"
 
@@ -1130,7 +1131,19 @@ void dist_check_peers(const DistData& D, cudaStream_t s) {
         uint64_t err = 0;
         EW_CUDA_CHECK(cudaMemcpyAsync(&err, P->mbox.get() + Mbox::err(D.nparts), sizeof(err), cudaMemcpyDeviceToHost, s));
         EW_CUDA_CHECK(cudaStreamSynchronize(s));
-        if (err) throw Error(EW_CUDA, "peer transport: a peer did not answer within ~30 s (rank failure?)");
+        if (err) {
+            // the mailbox at the time of the failure: which wait was stuck
+            const int32_t G = D.nparts;
+            std::vector<uint64_t> mb(3 * G), ep(2);
+            EW_CUDA_CHECK(cudaMemcpyAsync(mb.data(), P->mbox.get(), mb.size() * 8, cudaMemcpyDeviceToHost, s));
+            EW_CUDA_CHECK(cudaMemcpyAsync(ep.data(), P->epochs.get(), 16, cudaMemcpyDeviceToHost, s));
+            EW_CUDA_CHECK(cudaStreamSynchronize(s));
+            std::string m = "peer transport: a peer did not answer within ~30 s (rank failure?); partition " +
+                            std::to_string(P->part) + " epochs halo " + std::to_string(ep[0]) + " reduction " +
+                            std::to_string(ep[1]) + "; mailbox halo/ack/red:";
+            for (size_t i = 0; i < mb.size(); ++i) m += (i % G == 0 ? " |" : " ") + std::to_string(mb[i]);
+            throw Error(EW_CUDA, m);
+        }
     }
 }
 
@@ -1178,15 +1191,46 @@ void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s) {
     }
 }
 
-CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_config& cfg, double* x,
-                  cudaStream_t s) {
-    require(cfg.rel_tolerance > 0.0, "cg: tolerance must be positive");
-    require(cfg.max_iterations >= 0, "cg: max_iterations must be >= 0");
-    const int jacobi = cfg.jacobi ? 1 : 0;
-    if (jacobi) require(diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
-    int64_t off = 0;
+namespace {
+
+// One CG iteration k (cg.cpp:69-101) of every local partition on stream t;
+// k only selects the launch pattern (refresh), the kernels count iterations
+// on the device.
+void dist_iteration(DistData& D, const ew_cg_config& cfg, int jacobi, int64_t k, cudaStream_t t) {
+    spmv_exchange(D, &DistPart::p_ext, t, true, true);
+    reduce_finalize(D, cg::kPq, cfg, t);
+    const bool refresh = cfg.recompute_interval > 0 && k % cfg.recompute_interval == 0;
+    for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
+        if (mode < 0) break;
+        if (mode == 2) spmv_exchange(D, &DistPart::x_ext, t, true, false);
+        for (auto& P : D.parts) {
+            cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock, P->nloc),
+                                      cg::kRedBlock, 0, t>>>(
+                mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(), P->nloc,
+                jacobi, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(), P->st.get(), P->hist.get());
+            launched("cg::update_kernel<dist>");
+        }
+    }
+    reduce_finalize(D, cg::kUpdate, cfg, t);
     for (auto& P : D.parts) {
-        const int64_t n = P->nloc, ne = P->nloc + P->nghost;
+        cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, t>>>(
+            P->p_ext.get(), P->r.get(), P->diag.get(), P->nloc, jacobi, P->st.get());
+        launched("cg::p_kernel");
+    }
+}
+
+}  // namespace
+
+// Everything a solve with this configuration allocates or captures: the
+// working vectors, pinned polling slots and (device transports) the CUDA
+// graph of one refresh block. Kept on the operator; a later solve with the
+// same configuration does no allocation (cudaFree / cudaMallocHost can wait
+// for the whole device, which must not happen while peers spin on this
+// partition: ew_mgpu runs this for every partition before any solve starts).
+void dist_cg_setup(DistData& D, const ew_cg_config& cfg, cudaStream_t s) {
+    const int jacobi = cfg.jacobi ? 1 : 0;
+    for (auto& P : D.parts) {
+        const int64_t n = P->nloc;
         P->r.alloc(n);
         P->b.alloc(n);
         P->diag.alloc(jacobi ? n : 0);
@@ -1194,8 +1238,55 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         const int64_t spmv_blocks = (n + 255) / 256;
         P->partials.alloc(std::max<size_t>(2 * cg::kRedGridMax, cg::dot_partials(spmv_blocks)));
         P->tickets.alloc(std::max<size_t>(1, cg::dot_tickets(spmv_blocks)));
-        EW_CUDA_CHECK(cudaMemsetAsync(P->tickets.get(), 0, P->tickets.bytes(), s));
         P->st.alloc(1);
+    }
+    if (!D.hst) EW_CUDA_CHECK(cudaMallocHost(&D.hst, 2 * sizeof(cg::State)));
+    for (auto& e : D.poll_ev)
+        if (!e) EW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (D.use_nccl || cfg.max_iterations <= 0) return;
+    // device transports: one CUDA graph of a refresh block, replayed (the
+    // comm stream joins the capture through its events)
+    const int64_t interval = cfg.recompute_interval;
+    const int64_t B = interval > 0 ? interval : 32;
+    const int64_t hsize = static_cast<int64_t>(D.parts[0]->hist.size());
+    const bool same = D.exec && D.g_tol == cfg.rel_tolerance && D.g_div == cfg.divergence_limit &&
+                      D.g_interval == interval && D.g_jacobi == jacobi && D.g_hist == hsize;
+    if (same) return;
+    if (D.exec) cudaGraphExecDestroy(D.exec);
+    D.exec = nullptr;
+    if (!D.cap) EW_CUDA_CHECK(cudaStreamCreateWithFlags(&D.cap, cudaStreamNonBlocking));
+    const int64_t before = g_launches.load();
+    cudaGraph_t graph = nullptr;
+    EW_CUDA_CHECK(cudaStreamBeginCapture(D.cap, cudaStreamCaptureModeThreadLocal));
+    try {
+        for (int64_t k = 1; k <= B; ++k) dist_iteration(D, cfg, jacobi, k, D.cap);
+    } catch (...) {
+        cudaStreamEndCapture(D.cap, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    EW_CUDA_CHECK(cudaStreamEndCapture(D.cap, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&D.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    EW_CUDA_CHECK(e);
+    D.per_block = g_launches.load() - before;
+    g_launches.fetch_sub(D.per_block, std::memory_order_relaxed);  // counted per replay
+    D.g_tol = cfg.rel_tolerance, D.g_div = cfg.divergence_limit, D.g_interval = interval;
+    D.g_jacobi = jacobi, D.g_hist = hsize;
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_config& cfg, double* x,
+                  cudaStream_t s) {
+    require(cfg.rel_tolerance > 0.0, "cg: tolerance must be positive");
+    require(cfg.max_iterations >= 0, "cg: max_iterations must be >= 0");
+    const int jacobi = cfg.jacobi ? 1 : 0;
+    if (jacobi) require(diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+    dist_cg_setup(D, cfg, s);
+    int64_t off = 0;
+    for (auto& P : D.parts) {
+        const int64_t n = P->nloc, ne = P->nloc + P->nghost;
+        EW_CUDA_CHECK(cudaMemsetAsync(P->tickets.get(), 0, P->tickets.bytes(), s));
         EW_CUDA_CHECK(cudaMemsetAsync(P->st.get(), 0, sizeof(cg::State), s));
         const long long max_it = cfg.max_iterations;
         EW_CUDA_CHECK(cudaMemcpyAsync(&P->st.get()->max_it, &max_it, sizeof(max_it), cudaMemcpyHostToDevice, s));
@@ -1216,10 +1307,13 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
         launched("cg::init_kernel<dist>");
     }
     reduce_finalize(D, cg::kBnorm, cfg, s);
+    cg::State* hst = static_cast<cg::State*>(D.hst);
     std::vector<cg::State> hs(D.parts.size());
-    for (size_t i = 0; i < D.parts.size(); ++i)
-        EW_CUDA_CHECK(cudaMemcpyAsync(&hs[i], D.parts[i]->st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
-    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < D.parts.size(); ++i) {
+        EW_CUDA_CHECK(cudaMemcpyAsync(&hst[0], D.parts[i]->st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        hs[i] = hst[0];
+    }
     double flags[2] = {0.0, 0.0};
     for (auto& h : hs) {
         if (h.status == cg::kBadRhs) flags[0] = 1.0;
@@ -1259,111 +1353,44 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
     reduce_finalize(D, cg::kStart, cfg, s);
 
     DistPart& P0 = *D.parts[0];
-    // pinned polling slots and events kept on the operator (cudaMallocHost
-    // per solve can stall the device)
-    if (!D.hst) EW_CUDA_CHECK(cudaMallocHost(&D.hst, 2 * sizeof(cg::State)));
-    for (auto& e : D.poll_ev)
-        if (!e) EW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cg::State* hst = static_cast<cg::State*>(D.hst);
     cudaEvent_t* ev = D.poll_ev;
-    auto cleanup = [] {};
-    cg::State h{};
-    try {
-        // one CG iteration on stream t (cg.cpp:69-101); k only selects the
-        // launch pattern (refresh), the kernels count iterations on the device
-        auto iteration = [&](int64_t k, cudaStream_t t) {
-            spmv_exchange(D, &DistPart::p_ext, t, true, true);
-            reduce_finalize(D, cg::kPq, cfg, t);
-            const bool refresh = cfg.recompute_interval > 0 && k % cfg.recompute_interval == 0;
-            for (int mode : {refresh ? 1 : 0, refresh ? 2 : -1}) {
-                if (mode < 0) break;
-                if (mode == 2) spmv_exchange(D, &DistPart::x_ext, t, true, false);
-                for (auto& P : D.parts) {
-                    cg::update_kernel<true><<<cg::resident_grid(cg::update_kernel<true>, cg::kRedBlock, P->nloc),
-                                              cg::kRedBlock, 0, t>>>(
-                        mode, P->x_ext.get(), P->r.get(), P->p_ext.get(), P->q.get(), P->b.get(), P->diag.get(),
-                        P->nloc, jacobi, cfg.rel_tolerance, cfg.divergence_limit, P->partials.get(), P->st.get(),
-                        P->hist.get());
-                    launched("cg::update_kernel<dist>");
-                }
-            }
-            reduce_finalize(D, cg::kUpdate, cfg, t);
-            for (auto& P : D.parts) {
-                cg::p_kernel<<<cg::resident_grid(cg::p_kernel, 256, P->nloc), 256, 0, t>>>(
-                    P->p_ext.get(), P->r.get(), P->diag.get(), P->nloc, jacobi, P->st.get());
-                launched("cg::p_kernel");
-            }
-        };
-        // every rank launches the same blocks and stops on the same polled
-        // state (identical decisions everywhere), so the exchanges pair up
-        int j = 0;
-        auto poll = [&]() -> bool {
-            const int slot = j & 1;
-            EW_CUDA_CHECK(cudaMemcpyAsync(&hst[slot], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
-            EW_CUDA_CHECK(cudaEventRecord(ev[slot], s));
-            bool stop = false;
-            if (j > 0) {
-                EW_CUDA_CHECK(cudaEventSynchronize(ev[slot ^ 1]));
-                stop = hst[slot ^ 1].done != 0;
-            }
-            ++j;
-            return stop;
-        };
-        const int64_t interval = cfg.recompute_interval;
-        if (!D.use_nccl && cfg.max_iterations > 0) {
-            // device transports: one CUDA graph of a refresh block, replayed
-            // (the comm stream joins the capture through its events)
-            const int64_t B = interval > 0 ? interval : 32;
-            const int64_t hsize = static_cast<int64_t>(P0.hist.size());
-            const bool same = D.exec && D.g_tol == cfg.rel_tolerance && D.g_div == cfg.divergence_limit &&
-                              D.g_interval == interval && D.g_jacobi == jacobi && D.g_hist == hsize;
-            if (!same) {
-                if (D.exec) cudaGraphExecDestroy(D.exec);
-                D.exec = nullptr;
-                if (!D.cap) EW_CUDA_CHECK(cudaStreamCreateWithFlags(&D.cap, cudaStreamNonBlocking));
-                const int64_t before = g_launches.load();
-                cudaGraph_t graph = nullptr;
-                EW_CUDA_CHECK(cudaStreamBeginCapture(D.cap, cudaStreamCaptureModeThreadLocal));
-                try {
-                    for (int64_t k = 1; k <= B; ++k) iteration(k, D.cap);
-                } catch (...) {
-                    cudaStreamEndCapture(D.cap, &graph);
-                    if (graph) cudaGraphDestroy(graph);
-                    throw;
-                }
-                EW_CUDA_CHECK(cudaStreamEndCapture(D.cap, &graph));
-                const cudaError_t e = cudaGraphInstantiate(&D.exec, graph, 0);
-                cudaGraphDestroy(graph);
-                EW_CUDA_CHECK(e);
-                D.per_block = g_launches.load() - before;
-                g_launches.fetch_sub(D.per_block, std::memory_order_relaxed);  // counted per replay below
-                D.g_tol = cfg.rel_tolerance, D.g_div = cfg.divergence_limit, D.g_interval = interval;
-                D.g_jacobi = jacobi, D.g_hist = hsize;
-            }
-            const int64_t blocks = (cfg.max_iterations + B - 1) / B;
-            for (int64_t blk = 0; blk < blocks; ++blk) {
-                EW_CUDA_CHECK(cudaGraphLaunch(D.exec, s));
-                g_launches.fetch_add(D.per_block, std::memory_order_relaxed);
-                if (poll()) break;
-            }
-        } else {
-            int64_t it = 1;
-            int batch = 8;
-            while (it <= cfg.max_iterations) {
-                const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
-                for (; it <= last; ++it) iteration(it, s);
-                if (poll()) break;
-                batch = std::min(batch * 2, 64);
-            }
+    // every rank launches the same blocks and stops on the same polled
+    // state (identical decisions everywhere), so the exchanges pair up
+    int j = 0;
+    auto poll = [&]() -> bool {
+        const int slot = j & 1;
+        EW_CUDA_CHECK(cudaMemcpyAsync(&hst[slot], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaEventRecord(ev[slot], s));
+        bool stop = false;
+        if (j > 0) {
+            EW_CUDA_CHECK(cudaEventSynchronize(ev[slot ^ 1]));
+            stop = hst[slot ^ 1].done != 0;
         }
-        EW_CUDA_CHECK(cudaMemcpyAsync(&hst[0], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
-        EW_CUDA_CHECK(cudaStreamSynchronize(s));
-        h = hst[0];
-    } catch (...) {
-        cleanup();
-        throw;
+        ++j;
+        return stop;
+    };
+    const int64_t interval = cfg.recompute_interval;
+    if (!D.use_nccl && cfg.max_iterations > 0) {
+        const int64_t B = interval > 0 ? interval : 32;
+        const int64_t blocks = (cfg.max_iterations + B - 1) / B;
+        for (int64_t blk = 0; blk < blocks; ++blk) {
+            EW_CUDA_CHECK(cudaGraphLaunch(D.exec, s));
+            g_launches.fetch_add(D.per_block, std::memory_order_relaxed);
+            if (poll()) break;
+        }
+    } else {
+        int64_t it = 1;
+        int batch = 8;
+        while (it <= cfg.max_iterations) {
+            const int64_t last = std::min<int64_t>(cfg.max_iterations, it + batch - 1);
+            for (; it <= last; ++it) dist_iteration(D, cfg, jacobi, it, s);
+            if (poll()) break;
+            batch = std::min(batch * 2, 64);
+        }
     }
-    cleanup();
+    EW_CUDA_CHECK(cudaMemcpyAsync(&hst[0], P0.st.get(), sizeof(cg::State), cudaMemcpyDeviceToHost, s));
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    const cg::State h = hst[0];
     off = 0;
     for (auto& P : D.parts) {
         if (P->nloc) EW_CUDA_CHECK(cudaMemcpyAsync(x + off, P->x_ext.get(), P->nloc * 8, cudaMemcpyDeviceToDevice, s));
@@ -1372,6 +1399,185 @@ CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     dist_check_peers(D, s);
     return cg_outputs(h.status, h.iterations, cfg, P0.hist.get());
+}
+
+// ---- single process, several GPUs (SURVEY.md §8(b) ew_mgpu_cg_solve) --------
+// One DistData per partition, exactly as one rank of the CUDA-IPC transport
+// (the same push / mailbox / publish kernels, one partition per operator),
+// but the peers are this process's other partitions on other devices (or
+// the same one): their ghost buffers and mailboxes are plain device pointers
+// reached through peer access, and each partition's solve runs on its own
+// host thread and stream.
+struct MgpuData {
+    int32_t G = 0;
+    int64_t n = 0;
+    std::vector<int> dev;
+    std::vector<int64_t> bounds;
+    std::vector<std::shared_ptr<DistData>> parts;
+    std::vector<cudaStream_t> streams;
+    ~MgpuData() {
+        parts.clear();
+        for (size_t g = 0; g < streams.size(); ++g) {
+            cudaSetDevice(dev[g]);
+            cudaStreamDestroy(streams[g]);
+        }
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = 0;
+    DeviceGuard() { cudaGetDevice(&prev); }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Runs fn(g) for every partition on its own thread (device set), rethrowing
+// the first failure.
+template <typename Fn>
+void on_every_part(MgpuData& M, Fn&& fn) {
+    std::vector<std::exception_ptr> err(M.G);
+    std::vector<std::thread> th;
+    for (int32_t g = 0; g < M.G; ++g)
+        th.emplace_back([&, g] {
+            try {
+                EW_CUDA_CHECK(cudaSetDevice(M.dev[g]));
+                fn(g);
+            } catch (...) {
+                err[g] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
+std::shared_ptr<MgpuData> mgpu_create(int64_t n, const int64_t* ro, const int64_t* ci, const double* v,
+                                      int32_t G, const int32_t* devices, const std::string& kid,
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts) {
+    require(G >= 1, "mgpu: need at least one partition");
+    require(kid == "k1" || kid == "k2" || kid == "csr_ref",
+            "partitioned kernels: k1, k2 or csr_ref (the local matrix has ghost columns)");
+    int ndev = 0;
+    EW_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    DeviceGuard guard;
+    auto M = std::make_shared<MgpuData>();
+    M->G = G;
+    M->n = n;
+    for (int32_t g = 0; g < G; ++g) {
+        const int d = devices ? devices[g] : g;
+        require(d >= 0 && d < ndev, "mgpu: device " + std::to_string(d) + " does not exist");
+        M->dev.push_back(d);
+    }
+    M->bounds = partition_rows(ro, n, G);
+    // every partition's ghosts from the global CSR; peer access between the devices
+    std::vector<std::vector<int64_t>> ghosts(G);
+    for (int32_t h = 0; h < G; ++h) ghosts[h] = ghost_list(ro + M->bounds[h], ci, M->bounds[h], M->bounds[h + 1]);
+    for (int32_t a = 0; a < G; ++a)
+        for (int32_t b = 0; b < G; ++b) {
+            if (M->dev[a] == M->dev[b]) continue;
+            int ok = 0;
+            EW_CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, M->dev[a], M->dev[b]));
+            require(ok, "mgpu: device " + std::to_string(M->dev[a]) + " cannot access device " +
+                            std::to_string(M->dev[b]) + " (no peer access)");
+            EW_CUDA_CHECK(cudaSetDevice(M->dev[a]));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(M->dev[b], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            else EW_CUDA_CHECK(e);
+        }
+    for (int32_t g = 0; g < G; ++g) {
+        EW_CUDA_CHECK(cudaSetDevice(M->dev[g]));
+        cudaStream_t s = nullptr;
+        EW_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        M->streams.push_back(s);
+        std::vector<std::vector<int64_t>> needs(G);
+        for (int32_t h = 0; h < G; ++h) {
+            if (h == g) continue;
+            for (int64_t c : ghosts[h])
+                if (c >= M->bounds[g] && c < M->bounds[g + 1]) needs[h].push_back(c);
+        }
+        auto D = std::make_shared<DistData>();
+        D->nparts = G;
+        D->first = g;
+        D->nlocal = 1;
+        D->kernel_id = kid;
+        D->bounds = M->bounds;
+        auto P = std::make_unique<DistPart>();
+        build_part(*P, g, G, D->bounds, ro + M->bounds[g], ci, v, ghosts[g], needs, kid, cfg, opts, s);
+        if (G > 1) alloc_mailbox(*P, G, s);
+        D->parts.push_back(std::move(P));
+        M->parts.push_back(D);
+    }
+    if (G > 1) {
+        std::vector<double*> pp(G), px(G);
+        std::vector<uint64_t*> mb(G);
+        for (int32_t h = 0; h < G; ++h) {
+            DistPart& H = *M->parts[h]->parts[0];
+            pp[h] = H.p_ext.get();
+            px[h] = H.x_ext.get();
+            mb[h] = H.mbox.get();
+        }
+        for (int32_t g = 0; g < G; ++g) {
+            EW_CUDA_CHECK(cudaSetDevice(M->dev[g]));
+            DistPart& P = *M->parts[g]->parts[0];
+            std::vector<int64_t> tail(G, 0);
+            for (int32_t h = 0; h < G; ++h) {
+                if (h == g) continue;
+                const DistPart& H = *M->parts[h]->parts[0];
+                tail[h] = H.nloc + H.recv_off[g];
+            }
+            peer_plan(P, G, pp, px, mb, tail, M->streams[g]);
+            M->parts[g]->peer = M->parts[g]->ipc = true;  // one partition per operator, peers elsewhere
+        }
+    }
+    for (int32_t g = 0; g < G; ++g) {
+        EW_CUDA_CHECK(cudaSetDevice(M->dev[g]));
+        init_overlap(*M->parts[g]);
+        EW_CUDA_CHECK(cudaStreamSynchronize(M->streams[g]));
+    }
+    return M;
+}
+
+int64_t mgpu_rows(const MgpuData& M) { return M.n; }
+
+// y = A x, host vectors of n entries.
+void mgpu_spmv(MgpuData& M, const double* x, double* y) {
+    on_every_part(M, [&](int32_t g) {
+        const int64_t r0 = M.bounds[g], nl = M.bounds[g + 1] - r0;
+        const cudaStream_t s = M.streams[g];
+        Scratch<double> xd(nl, s), yd(nl, s);
+        if (nl) EW_CUDA_CHECK(cudaMemcpyAsync(xd.get(), x + r0, nl * 8, cudaMemcpyHostToDevice, s));
+        dist_spmv(*M.parts[g], xd.get(), yd.get(), s);
+        if (nl) EW_CUDA_CHECK(cudaMemcpyAsync(y + r0, yd.get(), nl * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        dist_check_peers(*M.parts[g], s);
+    });
+}
+
+// cg_solve over all partitions (host b, diag, x of n entries); every
+// partition takes the same decisions, partition 0 reports.
+CgOutputs mgpu_cg(MgpuData& M, const double* b, const double* diag, const ew_cg_config& cfg, double* x) {
+    const bool jac = cfg.jacobi != 0;
+    require(!jac || diag != nullptr, "cg: jacobi preconditioner needs the diagonal");
+    std::vector<CgOutputs> out(M.G);
+    // allocations and graph capture of every partition first: none of them
+    // may wait for the device while another partition's kernels spin
+    on_every_part(M, [&](int32_t g) { dist_cg_setup(*M.parts[g], cfg, M.streams[g]); });
+    on_every_part(M, [&](int32_t g) {
+        const int64_t r0 = M.bounds[g], nl = M.bounds[g + 1] - r0;
+        const cudaStream_t s = M.streams[g];
+        Scratch<double> bd(nl, s), dd(jac ? nl : 0, s), xd(nl, s);
+        if (nl) {
+            EW_CUDA_CHECK(cudaMemcpyAsync(bd.get(), b + r0, nl * 8, cudaMemcpyHostToDevice, s));
+            if (jac) EW_CUDA_CHECK(cudaMemcpyAsync(dd.get(), diag + r0, nl * 8, cudaMemcpyHostToDevice, s));
+        }
+        out[g] = dist_cg(*M.parts[g], bd.get(), jac ? dd.get() : nullptr, cfg, xd.get(), s);
+        if (nl) EW_CUDA_CHECK(cudaMemcpyAsync(x + r0, xd.get(), nl * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+    return out[0];
 }
 
 void nccl_unique_id(void* out) {

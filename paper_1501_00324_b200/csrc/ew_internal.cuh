@@ -463,6 +463,15 @@ void dist_check_peers(const DistData& D, cudaStream_t s);
 CgOutputs dist_cg(DistData& D, const double* b, const double* diag, const ew_cg_config& cfg, double* x,
                   cudaStream_t s);
 void nccl_unique_id(void* out);
+// Single process, several GPUs: partition g of the square host CSR on
+// devices[g] (NULL: device g), peers over peer access (ew_mgpu_*).
+struct MgpuData;
+std::shared_ptr<MgpuData> mgpu_create(int64_t n, const int64_t* ro, const int64_t* ci, const double* v,
+                                      int32_t nparts, const int32_t* devices, const std::string& kid,
+                                      const ew_warp_config& cfg, const ew_kernel_options& opts);
+int64_t mgpu_rows(const MgpuData& M);
+void mgpu_spmv(MgpuData& M, const double* x, double* y);
+CgOutputs mgpu_cg(MgpuData& M, const double* b, const double* diag, const ew_cg_config& cfg, double* x);
 
 // Final status -> exception or result (+ history copied back).
 CgOutputs cg_outputs(int status, long long iterations, const ew_cg_config& cfg, const double* hist_dev);

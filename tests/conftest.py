@@ -4,6 +4,11 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# Tests map several partitions of the multi-GPU paths onto one GPU, each
+# with its own streams whose kernels wait on each other's (spin-waits on
+# peer mailboxes): they need a hardware queue each, more than the default
+# 8 (set before the first CUDA context).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

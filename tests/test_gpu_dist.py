@@ -295,3 +295,54 @@ def test_bench_one_gpu_all_lines():
     c5 = line["cg"]
     assert c5["scaling"] == "strong" and c5["config"]["config"] == "c5" and c5["value"] > 0
     assert c5["config"]["iterations_run"] == [60, 60]
+
+
+@pytest.mark.parametrize("ngpus", [1, 2, 4])
+def test_mgpu_single_process_matches_partitioned(ew, R, ngpus):
+    """ew_mgpu_* (one process, one host thread + stream per block, peers
+    over peer access) with every block mapped onto this GPU: the same
+    partitions, kernels and rank-ordered sums as the in-process peer
+    transport, so SpMV bitwise the single-GPU K1 and the CG history, count
+    and solution bitwise those of Dist.local(..., transport="peer")."""
+    from oracle.oracle import Csr
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.elasticity_box(14, 13, 12)
+    m = Csr.make(n, n, ro, ci, v)
+    mg = ew.Mgpu(m, ngpus, devices=[0] * ngpus)
+    x = np.random.default_rng(7).uniform(-1, 1, n)
+    single = ew.Kernel("k1", ew.Csr(n, n, ro, ci, v)).apply(x)
+    y = mg.spmv(x)
+    both_zero = (y == 0) & (single == 0)
+    assert np.all(both_zero | (y.view(np.int64) == single.view(np.int64)))
+    b = R.spmv_csr(m, np.ones(n))
+    diag = R.extract_diagonal(m)
+    res = mg.cg_solve(b, diag, tol=1e-10, max_iterations=2000)
+    want = ew.Dist.local(m, ngpus, transport="peer" if ngpus > 1 else "copy").cg_solve(b, diag, tol=1e-10,
+                                                                                      max_iterations=2000)
+    assert res.converged and res.iterations == want.iterations
+    assert res.spmv_calls == 1 + res.iterations + res.iterations // 50
+    assert np.array_equal(res.residual_history.view(np.int64), want.residual_history.view(np.int64))
+    assert np.array_equal(res.solution.view(np.int64), want.solution.view(np.int64))
+    # against the reference (sequential dot products): the comparator
+    # (test_solver.cpp:104-112) until CG's amplification of rounding
+    # differences takes over (~200 iterations on these elasticity operators,
+    # as for the reference's own permuted-vs-plain pair), 1e-8 after
+    ref = R.cg_csr(m, b, tol=1e-10, max_iterations=2000)
+    assert res.iterations == ref.iterations
+    dev = np.abs(res.residual_history - ref.residual_history) / (1 + ref.residual_history)
+    assert np.all(dev[:150] <= 1e-10) and np.all(dev <= 1e-8)
+    assert np.max(np.abs(res.solution - ref.solution)) <= 1e-9
+
+
+def test_mgpu_errors(ew):
+    from oracle.oracle import Csr
+
+    m = Csr.make(3, 3, [0, 1, 2, 3], [0, 1, 5], [1.0, 1.0, 1.0])
+    with pytest.raises(ValueError):
+        ew.Mgpu(m, 1, devices=[0])  # column out of range
+    m = Csr.make(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    with pytest.raises(ValueError):
+        ew.Mgpu(m, 2, devices=[0, 99])  # no such device
+    with pytest.raises(ValueError):
+        ew.Mgpu(m, 1, devices=[0], kernel="k1rs")
