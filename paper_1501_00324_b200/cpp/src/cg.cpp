@@ -3,6 +3,7 @@
 #include "ellwarp/cg.hpp"
 
 #include <exception>
+#include <memory>
 
 namespace ellwarp {
 
@@ -101,6 +102,27 @@ CgResult cg_solve(const PreparedKernel& k, std::span<const real> b, const CgConf
 CgResult cg_solve_permuted(const PreparedKernel& k, std::span<const real> b, const CgConfig& cfg,
                            std::span<const real> diag) {
     return kernel_cg(k, b, cfg, diag, true);
+}
+
+CgResult cg_solve_multi_gpu(const SparseCsr& a, std::span<const real> b, const CgConfig& cfg,
+                            std::span<const real> diag, int ngpus, const std::string& kernel,
+                            std::span<const int> devices) {
+    require(a.square(), "cg: operator must be square");
+    require(cfg.rel_tolerance > 0.0, "cg: tolerance must be positive");
+    const idx n = a.nrows;
+    require(static_cast<idx>(b.size()) == n, "cg: operator must be square and match b");
+    check_diag(cfg, n, diag);
+    require(devices.empty() || static_cast<int>(devices.size()) == ngpus, "cg: one device per partition");
+    std::vector<int32_t> dev(devices.begin(), devices.end());
+    ew_mgpu h = nullptr;
+    device::check(ew_mgpu_create(n, a.row_offsets.data(), a.col_indices.data(), a.values.data(), ngpus,
+                                 dev.empty() ? nullptr : dev.data(), kernel.c_str(), nullptr, nullptr, &h));
+    std::unique_ptr<ew_mgpu_t, ew_status (*)(ew_mgpu)> guard(h, ew_mgpu_destroy);
+    const ew_cg_config c = to_c(cfg);
+    std::vector<real> x(n), hist(std::max<idx>(cfg.max_iterations, 0) + 1);
+    ew_cg_result r{};
+    device::check(ew_mgpu_cg_solve(h, b.data(), diag.empty() ? nullptr : diag.data(), &c, x.data(), hist.data(), &r));
+    return finish(std::move(x), hist, r);
 }
 
 AlphaAnalysis compute_alpha(real t_reorder, real t_kernel, real t_base) {

@@ -346,3 +346,21 @@ def test_mgpu_errors(ew):
         ew.Mgpu(m, 2, devices=[0, 99])  # no such device
     with pytest.raises(ValueError):
         ew.Mgpu(m, 1, devices=[0], kernel="k1rs")
+
+
+def test_reference_api_multi_gpu_cg(ew):
+    """The reference's Python entry (_ellwarp.cg_solve, module.cpp:227-249)
+    with the addition ngpus / devices: the row-partitioned solve from one
+    process (every block on this GPU here); same dict as the reference, the
+    single-GPU iteration count."""
+    from paper_1501_00324_b200 import load_ellwarp
+
+    e = load_ellwarp()
+    m = e.laplacian3d(12, 11, 10)
+    b = e.spmv_reference(m, [1.0] * m.nrows)
+    one = e.cg_solve(m, b, kernel="k1", tol=1e-8)
+    two = e.cg_solve(m, b, kernel="k1", tol=1e-8, devices=[0, 0, 0])
+    assert one["converged"] and two["converged"]
+    assert two["iterations"] == one["iterations"]
+    assert two["spmv_calls"] == one["spmv_calls"]
+    assert np.allclose(two["solution"], 1.0, atol=1e-6)
