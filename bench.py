@@ -662,7 +662,8 @@ def run_cg_dist(args, rank, world, local, shape="c2-slab"):
                    "step_ms_rank0": step_ms},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(per_gpu / hbm, 4),
-                     "traffic": ncu_traffic("c5/cg_k1_dot") if args.scale == 1.0 and not strong else None,
+                     "traffic": (ncu_traffic(f"c5/cg_k1_dot_strong/n{world}") if strong else ncu_traffic("c5/cg_k1_dot"))
+                     if args.scale == 1.0 else None,
                      "traffic_source": "profiles/ncu_traffic.json: DRAM bytes per launch of the iteration's dominant "
                                        "kernel, the fused SpMV + p.q (one per iteration)",
                      "algorithmic_bytes_per_iteration": b_it,

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1501_00324_b200 import capi, load_ellwarp, workloads as W  # noqa: E402
 
 ew_mod = load_ellwarp()
-only = set(sys.argv[1].split(",")) if len(sys.argv) > 1 else None
+only = set(sys.argv[1].split(",")) if len(sys.argv) > 1 and sys.argv[1] else None
 kids = sys.argv[2].split(",") if len(sys.argv) > 2 else ["k1", "k1rs", "k2:4", "k2:8", "k2:16", "csr_vector", "hyb"]
 for name, *_ in W.TABLE2:
     if only and name not in only:
