@@ -431,6 +431,22 @@ def run_spmv(args, rank, world, local):
     e2e_ms = max_over_ranks((time.perf_counter() - t) * 1e3 / k_e2e, world)
     e2e_val = world * eff_bytes / (e2e_ms * 1e-3) / 1e9
     calls_ms = np.array(calls) * 1e3
+    # this box's PCIe: the same bytes as one call's x upload and y download,
+    # plain pinned copies (context for the e2e number, which is copy-bound)
+    xg = torch.empty(nc, dtype=torch.float64, device="cuda")
+    yg = torch.empty(n, dtype=torch.float64, device="cuda")
+    pcie = {}
+    for name, fn, nbytes in (("h2d", lambda: xg.copy_(xh, non_blocking=True), 8 * nc),
+                             ("d2h", lambda: yh.copy_(yg, non_blocking=True), 8 * n)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(20):
+            fn()
+        torch.cuda.synchronize()
+        pcie[f"{name}_gbs"] = round(nbytes * 20 / (time.perf_counter() - t) / 1e9, 1)
+    del xg, yg
 
     out = {
         "metric": "SpMV effective GB/s (20 B/nnz, PAPER.md:553)",
@@ -467,7 +483,9 @@ def run_spmv(args, rank, world, local):
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
                 "call_ms_min_median_max": [round(float(calls_ms.min()), 4), round(float(np.median(calls_ms)), 4),
                                            round(float(calls_ms.max()), 4)],
-                "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y"},
+                "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y",
+                "pcie_copy_gbs": dict(pcie, note="plain pinned copies of one call's x (H2D) and y (D2H) bytes on "
+                                                 "this box, each direction alone")},
         "gpu_launches": int(launches),
         "clocks": dict(clk.summary(), window="1 s soak of the same launches right before the timed loop + the "
                                               "timed loop"),

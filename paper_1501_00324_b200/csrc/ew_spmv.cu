@@ -13,6 +13,7 @@
 // K2 combines lane partials with the reference's ascending-stride pairwise
 // tree (stride 1, 2, 4, ...), done here with __shfl_down_sync.
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "ew_cg.cuh"
@@ -289,8 +290,11 @@ __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
 // flight), the products go to shared memory, and warp 0 adds them in step
 // order. Same products (v * x[c], padding included), same sequential sum per
 // row as k1_kernel: bit-identical y.
+#ifndef EW_COOP8_MINB
+#define EW_COOP8_MINB 4
+#endif
 template <bool SCATTER, bool COMPACT, int H>
-__global__ void __launch_bounds__(32 * H) k1_coop_kernel(K1Args a) {
+__global__ void __launch_bounds__(32 * H, H == 8 ? EW_COOP8_MINB : 64 / (2 * H)) k1_coop_kernel(K1Args a) {
     constexpr int C = 8 * H;
     __shared__ double prod[2][C][32];
     pdl_wait();
@@ -350,6 +354,139 @@ __global__ void __launch_bounds__(32 * H) k1_coop_kernel(K1Args a) {
     pdl_trigger();
 }
 
+// ---- the same K1 with the warp's slab staged by the bulk-copy engine -------
+// k1_coop_kernel's loads (8 column + 8 value loads per lane and warp per
+// chunk, then the gathers) replaced by cp.async.bulk copies of whole chunks
+// of the layout warp's slab into shared memory (the slab is contiguous and
+// 256 / 128-byte aligned per warp, warp_layout.cpp:12-16), two chunks in
+// flight ahead of the one being multiplied, completion on an mbarrier: the
+// threads only gather x and multiply. Same products, same order: identical y.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <bool SCATTER, int H>
+__global__ void __launch_bounds__(32 * H) k1_bulk_kernel(K1Args a) {
+    constexpr int C = 8 * H;  // steps per chunk
+    extern __shared__ __align__(128) unsigned char k1b_smem[];
+    double* vals = reinterpret_cast<double*>(k1b_smem);                      // [2][C][32]
+    int32_t* cols = reinterpret_cast<int32_t*>(k1b_smem + 2 * C * 32 * 8);  // [2][C][32]
+    __shared__ __align__(8) uint64_t bar[2];
+    pdl_wait();
+    if (a.done && *a.done) return;  // uniform across the grid
+    const int64_t w = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (w << 5) + lane;
+    const int32_t mx = __ldg(a.maxrows + w);
+    const int64_t wo = __ldg(a.woff + w);
+    const int nchunks = (mx + C - 1) / C;
+    const uint64_t pol = evict_first_policy();
+    auto issue = [&](int c) {  // one thread: chunk c into stage c & 1
+        const int st = c & 1;
+        const int cnt = min(C, mx - c * C);
+        const uint32_t vb = static_cast<uint32_t>(cnt) * 256u, cb = static_cast<uint32_t>(cnt) * 128u;
+        mbar_expect_tx(&bar[st], vb + cb);
+        const int64_t s0 = wo + int64_t(c) * C * 32;
+        bulk_g2s(vals + st * C * 32, a.values + s0, vb, &bar[st], pol);
+        bulk_g2s(cols + st * C * 32, a.cols + s0, cb, &bar[st], pol);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int c = 0; c < min(2, nchunks); ++c) issue(c);
+    }
+    int64_t target = p;
+    if (SCATTER && warp == 0 && p < a.nrows) target = a.fwd[p];
+    __syncthreads();
+    uint64_t keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    double acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int st = c & 1;
+        mbar_wait(&bar[st], (c >> 1) & 1);
+        const int j0 = warp * 8, cnt = min(8, mx - c * C - j0);
+        double* v = vals + st * C * 32;
+        const int32_t* cl = cols + st * C * 32;
+        if (cnt > 0) {
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < cnt)
+                    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                                 : "=d"(xv[u])
+                                 : "l"(a.x + cl[(j0 + u) * 32 + lane]), "l"(keep));
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < cnt) v[(j0 + u) * 32 + lane] = __dmul_rn(v[(j0 + u) * 32 + lane], xv[u]);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int n = min(C, mx - c * C);
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, v[j * 32 + lane]);
+            __syncwarp();
+            if (lane == 0 && c + 2 < nchunks) {
+                // the generic-proxy reads / writes of this stage come before
+                // the bulk copy's writes into it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(c + 2);
+            }
+        }
+    }
+    if (warp == 0 && p < a.nrows) a.y[target] = p < a.n_active ? acc : 0.0;
+    pdl_trigger();
+}
+
+template <bool SCATTER>
+void launch_k1_bulk(const K1Args& a, int64_t nwarps, int h, cudaStream_t s) {
+    const unsigned g = static_cast<unsigned>(nwarps);
+    auto go = [&](auto kernel, int hh) {
+        const int smem = 2 * 8 * hh * 32 * 12;
+        static std::once_flag once[3];
+        std::call_once(once[hh == 2 ? 0 : (hh == 4 ? 1 : 2)],
+                       [&] { cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(g);
+        cfg.blockDim = dim3(32 * hh);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl_enabled() ? 1 : 0;
+        cuda_check(cudaLaunchKernelEx(&cfg, kernel, a), "cudaLaunchKernelEx(k1_bulk_kernel)");
+    };
+    if (h == 2) go(k1_bulk_kernel<SCATTER, 2>, 2);
+    else if (h == 4) go(k1_bulk_kernel<SCATTER, 4>, 4);
+    else go(k1_bulk_kernel<SCATTER, 8>, 8);
+    launched("k1_bulk_kernel");
+}
+
 // Warps per CTA of k1_coop_kernel for a layout, 0: the plain kernel. Sorted,
 // column-major ws = 32 int32-column layouts with under one wave of
 // one-thread-per-row CTAs (148 SMs x 2048 threads). H trades the chunks the
@@ -376,6 +513,8 @@ int coop_warps(const LayoutData& l) {
 template <bool SCATTER>
 void launch_k1_coop(const K1Args& a, int64_t nwarps, int h, bool compact, cudaStream_t s) {
     const unsigned g = static_cast<unsigned>(nwarps);
+    // (the default shared-memory carveout: a larger one shrinks L1, where
+    // half the x gathers hit -- protein 4,973 -> 1,600 GB/s effective)
     auto go = [&](auto kernel, int hh) { launch_pdl(kernel, g, 32 * hh, s, a); };
     if (compact) {
         if (h == 2) go(k1_coop_kernel<SCATTER, true, 2>, 2);
@@ -663,7 +802,16 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
              l.cols16.get(), l.col_base.get()};
         const bool rm = l.row_major != 0, sf = streams(l), c = l.compact != 0;
         if (const int h = coop_warps(l)) {
-            scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
+            // EW_K1_BULK=1: the bulk-copy staging form (A/B; needs the
+            // layout's 32-slot slab alignment, the default)
+            static const bool bulk = [] {
+                const char* e = std::getenv("EW_K1_BULK");
+                return e && e[0] == '1';
+            }();
+            if (bulk && !c && l.align && l.segment_bytes == 128)
+                scatter ? launch_k1_bulk<true>(a, l.nwarps, h, s) : launch_k1_bulk<false>(a, l.nwarps, h, s);
+            else
+                scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
             return;
         }
         if (l.sorted) {

@@ -15,6 +15,13 @@ k = capi.Kernel("k1", a)
 x = torch.empty(nc, dtype=torch.float64, pin_memory=True); x.copy_(torch.rand(nc, dtype=torch.float64))
 y = torch.empty(n, dtype=torch.float64, pin_memory=True)
 xn, yn = x.numpy(), y.numpy()
+if os.environ.get("EW_SOAK"):
+    xd = torch.tensor(xn, device="cuda"); yd = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+    t = time.perf_counter()
+    while time.perf_counter() - t < float(os.environ["EW_SOAK"]):
+        for _ in range(50): k.apply(xd, yd, stream=st)
+        torch.cuda.synchronize()
 for _ in range(5): k.apply(xn, yn)
 for rep in range(3):
     t = time.perf_counter()
