@@ -446,6 +446,20 @@ def run_spmv(args, rank, world, local):
             fn()
         torch.cuda.synchronize()
         pcie[f"{name}_gbs"] = round(nbytes * 20 / (time.perf_counter() - t) / 1e9, 1)
+    # both directions at once on two streams (what the pipelined call needs):
+    # the floor of one call is (x + y bytes) / this aggregate rate
+    s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(20):
+        with torch.cuda.stream(s_up):
+            xg.copy_(xh, non_blocking=True)
+        with torch.cuda.stream(s_dn):
+            yh.copy_(yg, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    pcie["both_gbs"] = round((8 * nc + 8 * n) * 20 / dt / 1e9, 1)
+    pcie["call_floor_ms"] = round(dt / 20 * 1e3, 4)
     del xg, yg
 
     out = {
@@ -485,7 +499,8 @@ def run_spmv(args, rank, world, local):
                                            round(float(calls_ms.max()), 4)],
                 "path": "ew_kernel_apply(EW_MEM_HOST), pinned host x/y",
                 "pcie_copy_gbs": dict(pcie, note="plain pinned copies of one call's x (H2D) and y (D2H) bytes on "
-                                                 "this box, each direction alone")},
+                                                 "this box: each direction alone, and both at once (call_floor_ms: "
+                                                 "the copies of one call with nothing else to do)")},
         "gpu_launches": int(launches),
         "clocks": dict(clk.summary(), window="1 s soak of the same launches right before the timed loop + the "
                                               "timed loop"),
