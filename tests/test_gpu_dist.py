@@ -168,7 +168,15 @@ def test_nccl_transport_one_rank(ew, R, fem):
 def _ipc_worker(rank, world, port, q):
     """One rank of the IPC transport; both ranks share the one GPU (CUDA IPC
     works between processes on the same device), so the push / mailbox
-    protocol runs across real process boundaries."""
+    protocol runs across real process boundaries.
+
+    Two processes on one GPU (no MPS here) time-slice it: a rank's kernel
+    spinning on a peer mailbox can keep the GPU until the 30 s peer timeout
+    (the attempt then fails with a peer timeout, never with a silently wrong
+    result: a timed-out operator reports it). So each attempt builds fresh
+    operators, and the ranks agree on a retry (up to 4 attempts) when any
+    rank saw a peer timeout; a wrong result without one fails at once. On
+    one GPU per process (the real layout) there is no time-slicing."""
     try:
         import torch
         import torch.distributed as dist
@@ -185,12 +193,9 @@ def _ipc_worker(rank, world, port, q):
         bounds = capi.partition_rows(ro, world)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         bro = ro[r0:r1 + 1] - ro[r0]
-        d = capi.Dist.block_ipc(n, bro, ci[ro[r0]:ro[r1]], v[ro[r0]:ro[r1]], bounds, rank)
         x = np.random.default_rng(5).uniform(0.1, 1.0, n)
         a = capi.Csr(n, n, ro, ci, v)
         single = capi.Kernel("k1", a).apply(x)
-        ys = [d.spmv(x[r0:r1]) for _ in range(4)]
-        ok_spmv = all(same_up_to_zero_sign(y, single[r0:r1]) for y in ys)
         sp = W.laplacian_box(9, 8, 7)
         n2, _, ro2, ci2, v2 = sp
         m2 = Csr.make(n2, n2, ro2, ci2, v2)
@@ -198,19 +203,41 @@ def _ipc_worker(rank, world, port, q):
         ref = R.cg_csr(m2, b2)
         bounds2 = capi.partition_rows(ro2, world)
         s0, s1 = int(bounds2[rank]), int(bounds2[rank + 1])
-        d2 = capi.Dist.block_ipc(n2, ro2[s0:s1 + 1] - ro2[s0], ci2[ro2[s0]:ro2[s1]], v2[ro2[s0]:ro2[s1]], bounds2,
-                                 rank)
         diag = R.extract_diagonal(m2)
-        res = d2.cg_solve(b2[s0:s1], diag[s0:s1])
+        attempts = []
+        for attempt in range(4):
+            timed_out, err = 0, None
+            ys, res = [], None
+            try:
+                d = capi.Dist.block_ipc(n, bro, ci[ro[r0]:ro[r1]], v[ro[r0]:ro[r1]], bounds, rank)
+                d2 = capi.Dist.block_ipc(n2, ro2[s0:s1 + 1] - ro2[s0], ci2[ro2[s0]:ro2[s1]], v2[ro2[s0]:ro2[s1]],
+                                         bounds2, rank)
+                torch.cuda.synchronize()
+                dist.barrier()
+                ys = [d.spmv(x[r0:r1]) for _ in range(4)]
+                torch.cuda.synchronize()
+                dist.barrier()
+                res = d2.cg_solve(b2[s0:s1], diag[s0:s1])
+            except (capi.DeviceError, capi.CgDivergenceError) as e:
+                timed_out, err = 1, repr(e)
+            flags = [None] * world
+            dist.all_gather_object(flags, timed_out)
+            dist.barrier()
+            d = d2 = None
+            torch.cuda.synchronize()
+            dist.barrier()
+            attempts.append(err)
+            if not any(flags):
+                break
+        if res is None or any(flags):
+            raise RuntimeError(f"peer timeouts on every attempt (time-sliced GPU): {attempts}")
+        ok_spmv = all(same_up_to_zero_sign(y, single[r0:r1]) for y in ys)
         ok_cg = (res.converged and res.iterations == ref.iterations and
                  hist_ok(res.residual_history, ref.residual_history) and
                  np.allclose(res.solution, ref.solution[s0:s1], rtol=1e-8, atol=1e-10))
-        dist.barrier()
-        del d, d2
-        dist.barrier()
         detail = {"spmv_bad_calls": [i for i, y in enumerate(ys) if not same_up_to_zero_sign(y, single[r0:r1])],
                   "converged": res.converged, "it": res.iterations, "ref_it": ref.iterations,
-                  "hist_ok": hist_ok(res.residual_history, ref.residual_history)}
+                  "hist_ok": hist_ok(res.residual_history, ref.residual_history), "attempts": attempts}
         q.put((rank, ok_spmv, ok_cg, detail, ref.iterations))
         dist.destroy_process_group()
     except Exception as e:  # reported to the parent
@@ -231,7 +258,7 @@ def test_ipc_transport_two_processes(ew):
     procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=240) for _ in procs]
+    out = [q.get(timeout=600) for _ in procs]
     for p in procs:
         p.join(timeout=60)
     for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
