@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libellwarp_b200.so")
+# EW_B200_LIB: another build of the in-tree library (A/B runs of kernel variants)
+LIB_PATH = os.environ.get("EW_B200_LIB") or os.path.join(HERE, "lib", "libellwarp_b200.so")
 
 EW_OK, EW_INVALID_ARGUMENT, EW_CG_DIVERGENCE, EW_UNSUPPORTED, EW_CUDA, EW_OUT_OF_MEMORY = range(6)
 EW_MEM_HOST, EW_MEM_DEVICE = 0, 1
