@@ -489,7 +489,8 @@ void launch_k1_bulk(const K1Args& a, int64_t nwarps, int h, cudaStream_t s) {
 
 // Warps per CTA of k1_coop_kernel for a layout, 0: the plain kernel. Sorted,
 // column-major ws = 32 int32-column layouts with under one wave of
-// one-thread-per-row CTAs (148 SMs x 2048 threads). H trades the chunks the
+// one-thread-per-row CTAs (148 SMs x 2048 threads), unless they are over
+// half a wave of rows of at most 32 entries. H trades the chunks the
 // longest warp walks in sequence (ceil(max_mx / 8H)) against resident CTAs
 // (~32 / H per SM): layouts with a row over 96 entries take 8, small ones
 // (<= 8 CTAs per SM at H = 4) 4, the rest 2 -- the best or within 5% of the
@@ -505,6 +506,10 @@ int coop_warps(const LayoutData& l) {
         return 0;
     if (mode == 2 || mode == 4 || mode == 8) return mode;  // A/B: a fixed H
     if (l.nrows > int64_t{148} * 2048 || l.compact) return 0;
+    // over half a wave of short rows only (config 1: 262k rows of 5-15):
+    // the plain kernel's chains are short and its grid fills the GPU
+    // (5.8 us vs 10.7 us for H = 2)
+    if (l.nrows > int64_t{148} * 1024 && l.max_mx > 0 && l.max_mx <= 32) return 0;
     if (l.max_mx > 96) return 8;
     if (l.nwarps <= 148 * 8) return 4;
     return 2;
