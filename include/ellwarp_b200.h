@@ -343,6 +343,15 @@ ew_status ew_dist_create_block_ipc(int64_t nrows_global, int64_t nrows_local, co
                                    int32_t nparts, int32_t rank, ew_allgather_fn allgather, void* user,
                                    const char* kernel_id, const ew_warp_config* cfg,
                                    const ew_kernel_options* opts, void* stream, ew_dist* out);
+/* The setup exchange of ew_dist_create_block_ipc for this rank's row block,
+ * on the host only (no device work; a collective through the allgather):
+ * the block's ghost columns (ascending, hence grouped by owner) and, per peer
+ * h, the global rows of this block h needs, send_rows[send_off[h],
+ * send_off[h+1]). ghosts: capacity >= row_offsets[nrows_local]; send_off:
+ * nparts + 1; send_rows: capacity >= nrows_local * nparts. */
+ew_status ew_dist_plan_block(int64_t nrows_local, const int64_t* row_offsets, const int64_t* col_indices,
+                             const int64_t* bounds, int32_t nparts, int32_t rank, ew_allgather_fn allgather,
+                             void* user, int64_t* nghost, int64_t* ghosts, int64_t* send_off, int64_t* send_rows);
 ew_status ew_dist_destroy(ew_dist d);
 /* Row range, ghost count and send count of local partition i. */
 ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* row_begin, int64_t* row_end,

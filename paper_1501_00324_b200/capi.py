@@ -172,6 +172,8 @@ _SIGS = {
     "ew_dist_create_block_ipc": (C.c_int, [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, C.c_int32, C.c_int32,
                                            _vp, _vp, C.c_char_p, C.POINTER(WarpConfig),
                                            C.POINTER(KernelOptions), _vp, C.POINTER(_vp)]),
+    "ew_dist_plan_block": (C.c_int, [C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _i64p, _vp, _vp,
+                                     _vp]),
     "ew_dist_destroy": (C.c_int, [_vp]),
     "ew_dist_get_info": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, _i64p]),
     "ew_dist_spmv": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
@@ -671,6 +673,41 @@ def torch_allgather(data: bytes):
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, data)
     return out
+
+
+def dist_plan_block(ro, ci, bounds, rank, allgather=None):
+    """The setup exchange of Dist.block_ipc on the host (ew_dist_plan_block):
+    this rank's ghost columns and, per peer, the rows of this block it
+    sends. allgather(bytes) -> list of bytes in rank order (default:
+    torch.distributed). Collective; no device work."""
+    ro, ci, b = _host(ro, np.int64), _host(ci, np.int64), _host(bounds, np.int64)
+    G = b.size - 1
+    nloc = ro.size - 1
+    fn = allgather or torch_allgather
+    err = []
+
+    def cb(send, recv, nbytes, user):
+        try:
+            buf = b"".join(fn(C.string_at(send, nbytes)))
+            if len(buf) != nbytes * G:
+                raise ValueError("allgather returned the wrong size")
+            C.memmove(recv, buf, len(buf))
+            return 0
+        except Exception as e:  # reported through the status code
+            err.append(e)
+            return 1
+
+    cfn = ALLGATHER_FN(cb)
+    nghost = C.c_int64()
+    ghosts = np.empty(max(1, int(ro[-1])), np.int64)
+    send_off = np.empty(G + 1, np.int64)
+    send_rows = np.empty(max(1, nloc * G), np.int64)
+    st = lib().ew_dist_plan_block(nloc, _ptr(ro), _ptr(ci), _ptr(b), G, int(rank), C.cast(cfn, C.c_void_p), None,
+                                  C.byref(nghost), _ptr(ghosts), _ptr(send_off), _ptr(send_rows))
+    if err:
+        raise err[0]
+    check(st)
+    return ghosts[: nghost.value].copy(), [send_rows[send_off[h]:send_off[h + 1]].copy() for h in range(G)]
 
 
 class Dist:

@@ -731,6 +731,29 @@ ew_status ew_dist_create_block_ipc(int64_t nrows_global, int64_t nrows_local, co
     });
 }
 
+ew_status ew_dist_plan_block(int64_t nrows_local, const int64_t* row_offsets, const int64_t* col_indices,
+                             const int64_t* bounds, int32_t nparts, int32_t rank, ew_allgather_fn allgather,
+                             void* user, int64_t* nghost, int64_t* ghosts, int64_t* send_off, int64_t* send_rows) {
+    return guarded([&] {
+        ew::require(row_offsets != nullptr && bounds != nullptr && allgather != nullptr && nghost != nullptr &&
+                        ghosts != nullptr && send_off != nullptr && send_rows != nullptr,
+                    "null argument");
+        ew::require(nparts >= 1, "bad partition count");
+        std::vector<int64_t> b(bounds, bounds + nparts + 1);
+        for (int32_t g = 0; g < nparts; ++g) ew::require(b[g] <= b[g + 1], "partition bounds must be sorted");
+        ew::require(b[0] == 0, "partition bounds must start at 0");
+        ew::require(row_offsets[nrows_local] == 0 || col_indices != nullptr, "col_indices is null");
+        const ew::BlockPlan plan = ew::block_plan(nrows_local, row_offsets, col_indices, b, rank, allgather, user);
+        *nghost = static_cast<int64_t>(plan.ghosts.size());
+        std::copy(plan.ghosts.begin(), plan.ghosts.end(), ghosts);
+        send_off[0] = 0;
+        for (int32_t h = 0; h < nparts; ++h) {
+            std::copy(plan.needs[h].begin(), plan.needs[h].end(), send_rows + send_off[h]);
+            send_off[h + 1] = send_off[h] + static_cast<int64_t>(plan.needs[h].size());
+        }
+    });
+}
+
 ew_status ew_dist_destroy(ew_dist d) {
     return guarded([&] { delete d; });
 }

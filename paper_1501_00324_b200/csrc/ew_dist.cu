@@ -1031,6 +1031,49 @@ std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro,
     return D;
 }
 
+// The setup exchange of one rank's row block (host only, the caller's
+// allgather): its ghost list (columns outside the block, ascending, so
+// grouped by owner) and, per peer, the global rows that peer needs from this
+// block (ascending). counts[h * G + g]: how many of h's ghosts g owns.
+BlockPlan block_plan(int64_t nloc, const int64_t* bro, const int64_t* bci, const std::vector<int64_t>& bounds,
+                     int32_t rank, ew_allgather_fn allgather, void* user) {
+    const int32_t G = static_cast<int32_t>(bounds.size()) - 1;
+    require(G >= 1 && rank >= 0 && rank < G, "bad rank");
+    require(bounds[rank + 1] - bounds[rank] == nloc, "row block does not match the bounds");
+    auto ag = [&](const void* send, void* recv, size_t bytes) {
+        if (allgather(send, recv, bytes, user) != 0) throw Error(EW_INVALID_ARGUMENT, "allgather callback failed");
+    };
+    const int64_t r0 = bounds[rank], r1 = bounds[rank + 1];
+    const int64_t nglobal = bounds[G];
+    for (int64_t k = bro[0]; k < bro[nloc]; ++k)
+        require(bci[k] >= 0 && bci[k] < nglobal, "column out of range");
+    BlockPlan plan;
+    plan.ghosts = ghost_list(bro, bci, r0, r1);
+    // ghost requests: counts per owner, then the (owner-grouped, ascending) ids
+    std::vector<int64_t> my_need(G, 0);
+    plan.counts.assign(static_cast<size_t>(G) * G, 0);
+    for (int64_t c : plan.ghosts) my_need[owner_of(bounds, c)]++;
+    ag(my_need.data(), plan.counts.data(), G * sizeof(int64_t));
+    int64_t maxg = 1;
+    for (int32_t h = 0; h < G; ++h) {
+        int64_t t = 0;
+        for (int32_t g = 0; g < G; ++g) t += plan.counts[static_cast<size_t>(h) * G + g];
+        maxg = std::max(maxg, t);
+    }
+    std::vector<int64_t> mine(maxg, -1), every(static_cast<size_t>(G) * maxg);
+    std::copy(plan.ghosts.begin(), plan.ghosts.end(), mine.begin());
+    ag(mine.data(), every.data(), maxg * sizeof(int64_t));
+    plan.needs.assign(G, {});
+    for (int32_t h = 0; h < G; ++h) {
+        if (h == rank) continue;
+        int64_t skip = 0;  // h's ghosts owned by ranks < rank
+        for (int32_t g = 0; g < rank; ++g) skip += plan.counts[static_cast<size_t>(h) * G + g];
+        const int64_t* lst = every.data() + static_cast<size_t>(h) * maxg + skip;
+        plan.needs[h].assign(lst, lst + plan.counts[static_cast<size_t>(h) * G + rank]);
+    }
+    return plan;
+}
+
 std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* bro, const int64_t* bci,
                                                 const double* bv, const int64_t* bounds, int32_t nparts,
                                                 int32_t rank, ew_allgather_fn allgather, void* user,
@@ -1052,32 +1095,15 @@ std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* 
     auto ag = [&](const void* send, void* recv, size_t bytes) {
         if (allgather(send, recv, bytes, user) != 0) throw Error(EW_INVALID_ARGUMENT, "allgather callback failed");
     };
-    const int64_t r0 = D->bounds[rank], r1 = D->bounds[rank + 1];
-    const std::vector<int64_t> ghosts = ghost_list(bro, bci, r0, r1);
-    // ghost requests: counts per owner, then the (owner-grouped, ascending) ids
-    std::vector<int64_t> my_need(G, 0), all(static_cast<size_t>(G) * G);
-    for (int64_t c : ghosts) my_need[owner_of(D->bounds, c)]++;
-    ag(my_need.data(), all.data(), G * sizeof(int64_t));
-    int64_t maxg = 1;
-    for (int32_t h = 0; h < G; ++h) {
-        int64_t t = 0;
-        for (int32_t g = 0; g < G; ++g) t += all[static_cast<size_t>(h) * G + g];
-        maxg = std::max(maxg, t);
-    }
-    std::vector<int64_t> mine(maxg, -1), every(static_cast<size_t>(G) * maxg);
-    std::copy(ghosts.begin(), ghosts.end(), mine.begin());
-    ag(mine.data(), every.data(), maxg * sizeof(int64_t));
+    const int64_t nloc = D->bounds[rank + 1] - D->bounds[rank];
+    BlockPlan plan = block_plan(nloc, bro, bci, D->bounds, rank, allgather, user);
+    const std::vector<int64_t>& ghosts = plan.ghosts;
+    const std::vector<std::vector<int64_t>>& needs = plan.needs;
     auto before = [&](int32_t h, int32_t owner) {  // h's ghosts owned by ranks < owner
         int64_t t = 0;
-        for (int32_t g = 0; g < owner; ++g) t += all[static_cast<size_t>(h) * G + g];
+        for (int32_t g = 0; g < owner; ++g) t += plan.counts[static_cast<size_t>(h) * G + g];
         return t;
     };
-    std::vector<std::vector<int64_t>> needs(G);
-    for (int32_t h = 0; h < G; ++h) {
-        if (h == rank) continue;
-        const int64_t* lst = every.data() + static_cast<size_t>(h) * maxg + before(h, rank);
-        needs[h].assign(lst, lst + all[static_cast<size_t>(h) * G + rank]);
-    }
     auto P = std::make_unique<DistPart>();
     build_part(*P, rank, nparts, D->bounds, bro, bci, bv, ghosts, needs, kid, cfg, opts, s);
     if (G > 1) {

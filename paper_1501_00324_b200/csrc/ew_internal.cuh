@@ -451,6 +451,13 @@ std::shared_ptr<DistData> dist_create_block_ipc(int64_t nglobal, const int64_t* 
                                                 int32_t rank, ew_allgather_fn allgather, void* user,
                                                 const std::string& kid, const ew_warp_config& cfg,
                                                 const ew_kernel_options& opts, cudaStream_t s);
+struct BlockPlan {
+    std::vector<int64_t> ghosts;                // ascending global ids outside the block
+    std::vector<int64_t> counts;                // [h * G + g]: h's ghosts owned by g
+    std::vector<std::vector<int64_t>> needs;    // per peer: rows of this block it needs
+};
+BlockPlan block_plan(int64_t nloc, const int64_t* bro, const int64_t* bci, const std::vector<int64_t>& bounds,
+                     int32_t rank, ew_allgather_fn allgather, void* user);
 std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro, const int64_t* bci,
                                             const double* bv, const int64_t* bounds, int32_t nparts, int32_t rank,
                                             const void* nccl_id, const std::string& kid, const ew_warp_config& cfg,

@@ -161,3 +161,63 @@ def test_two_rank_partitioned_spmv_and_cg(R, F):
     assert np.all(np.abs(hist - ref.residual_history) <= 1e-10 * (1 + ref.residual_history))
     xs = np.concatenate([o[3] for o in out])
     assert np.allclose(xs, ref.solution, rtol=1e-8, atol=1e-10)
+
+
+def _plan_worker(rank, world, port, queue):
+    """One rank of the library's own IPC setup exchange (ew_dist_plan_block:
+    ghost list, counts all-gathered, ghost ids all-gathered, per-peer send
+    lists) over torch.distributed gloo: the code ew_dist_create_block_ipc
+    runs before any device work."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle.oracle import Reference
+    from paper_1501_00324_b200 import capi
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        m = Reference().fem_tet_graph(3000, 5, 21, 12)
+        bounds = capi.partition_rows(m.row_offsets, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        ro = m.row_offsets[r0:r1 + 1] - m.row_offsets[r0]
+        ci = m.col_indices[m.row_offsets[r0]:m.row_offsets[r1]]
+        ghosts, sends = capi.dist_plan_block(ro, ci, bounds, rank)
+        queue.put((rank, bounds.tolist(), ghosts.tolist(), [s.tolist() for s in sends]))
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        queue.put((rank, None, repr(e), None))
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_library_ipc_setup_exchange(F, world):
+    """ew_dist_plan_block from `world` processes (gloo allgather): every
+    rank's ghost list is the ascending set of its block's columns outside
+    the block, and what rank g sends to h is exactly the part of h's ghost
+    list that g owns."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(60)
+    for o in out:
+        assert o[1] is not None, o[2]
+    m = F.fem_tet_graph(3000, 5, 21, 12)
+    bounds = np.asarray(out[0][1])
+    for g in range(world):
+        r0, r1 = bounds[g], bounds[g + 1]
+        cols = m.col_indices[m.row_offsets[r0]:m.row_offsets[r1]]
+        want = np.unique(cols[(cols < r0) | (cols >= r1)])
+        assert np.array_equal(np.asarray(out[g][2], np.int64), want)
+    for g in range(world):
+        for h in range(world):
+            gh = np.asarray(out[h][2], np.int64)
+            owned = gh[(gh >= bounds[g]) & (gh < bounds[g + 1])] if h != g else np.zeros(0, np.int64)
+            assert np.array_equal(np.asarray(out[g][3][h], np.int64), owned), (g, h)
+    assert sum(len(s) for o in out for s in o[3]) > 0
