@@ -1442,11 +1442,18 @@ struct MgpuData {
     std::vector<std::shared_ptr<DistData>> parts;
     std::vector<cudaStream_t> streams;
     ~MgpuData() {
-        parts.clear();
+        int prev = 0;
+        cudaGetDevice(&prev);
+        // each block's buffers, graph and streams with its own device current
+        for (size_t g = 0; g < parts.size(); ++g) {
+            cudaSetDevice(dev[g]);
+            parts[g].reset();
+        }
         for (size_t g = 0; g < streams.size(); ++g) {
             cudaSetDevice(dev[g]);
             cudaStreamDestroy(streams[g]);
         }
+        cudaSetDevice(prev);
     }
 };
 
