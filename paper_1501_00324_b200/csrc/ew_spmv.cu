@@ -626,8 +626,12 @@ struct K2Args {
 // contiguous chunk of maxrows slots, then the ascending-stride tree.
 // DOT (the CG's fused p.q): each row's leader adds x[target] * y[target];
 // one partial per hardware warp, summed by cg::dot_final_kernel.
+// 40 registers (6 CTAs of 256 per SM; 48 unbounded, 5 CTAs): the lanes'
+// short chains are latency bound, so resident warps pay -- suite, same box:
+// harbor 2,948 -> 4,473, protein 3,851 -> 5,297, webbase 1,069 -> 1,303 GB/s
+// effective (32 registers / 8 CTAs: 3,647, 4,200, 807).
 template <bool SORTED, bool SCATTER, bool DOT = false>
-__global__ void __launch_bounds__(256) k2_kernel(K2Args a, double* __restrict__ partials) {
+__global__ void __launch_bounds__(256, 6) k2_kernel(K2Args a, double* __restrict__ partials) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t w = t >> a.ws_log2;
     const int32_t lane = static_cast<int32_t>(t & (a.ws - 1));
