@@ -293,8 +293,15 @@ __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
 #ifndef EW_COOP8_MINB
 #define EW_COOP8_MINB 4
 #endif
+#ifndef EW_COOP4_MINB
+#define EW_COOP4_MINB 8
+#endif
+#ifndef EW_COOP2_MINB
+#define EW_COOP2_MINB 16
+#endif
 template <bool SCATTER, bool COMPACT, int H>
-__global__ void __launch_bounds__(32 * H, H == 8 ? EW_COOP8_MINB : 64 / (2 * H)) k1_coop_kernel(K1Args a) {
+__global__ void __launch_bounds__(32 * H, H == 8 ? EW_COOP8_MINB : (H == 4 ? EW_COOP4_MINB : EW_COOP2_MINB))
+    k1_coop_kernel(K1Args a) {
     constexpr int C = 8 * H;
     __shared__ double prod[2][C][32];
     pdl_wait();
