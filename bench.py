@@ -381,10 +381,10 @@ def run_spmv(args, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         # the timed loop is a few ms (shorter than one nvidia-smi sample):
-        # the sampler records the clocks over a >= 1 s soak of the same
+        # the sampler records the clocks over a 0.5 s soak of the same
         # launches right before it, on the same stream, without a gap
         t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 1.0:
+        while time.perf_counter() - t_soak < 0.5:
             for _ in range(50):
                 apply(x, y, stream=stream)
             torch.cuda.current_stream().synchronize()
@@ -502,7 +502,7 @@ def run_spmv(args, rank, world, local):
                                                  "this box: each direction alone, and both at once (call_floor_ms: "
                                                  "the copies of one call with nothing else to do)")},
         "gpu_launches": int(launches),
-        "clocks": dict(clk.summary(), window="1 s soak of the same launches right before the timed loop + the "
+        "clocks": dict(clk.summary(), window="0.5 s soak of the same launches right before the timed loop + the "
                                               "timed loop"),
         "prepare_s": round(t_prepare, 3),
     }
