@@ -410,7 +410,7 @@ def run_spmv(args, rank, world, local):
     # warps (compact_layout), int32 elsewhere, padding slots included
     kinfo = k.info()
     slots, narrow = int(kinfo.stored_slots), int(kinfo.narrow_slots)
-    streamed = 8 * slots + 2 * narrow + 4 * (slots - narrow) + 8 * n + 8 * nc
+    streamed = 8 * slots + int(kinfo.col_stream_bytes) + 8 * n + 8 * nc
     streamed_gbs = streamed / (kern_ms * 1e-3) / 1e9 if kern_ms else None
 
     # end-to-end through the C ABI with pinned host buffers
@@ -491,8 +491,10 @@ def run_spmv(args, rank, world, local):
                      "streamed_bytes_per_launch": streamed,
                      "streamed_frac": round(streamed_gbs / hbm, 4) if streamed_gbs else None,
                      "note": "achieved/frac: the reference format's bytes (12 B/nnz + 8 n + 8 ncols, SURVEY 8d) "
-                             "over the kernel time; streamed_frac: the bytes this layout moves (16-bit columns "
-                             "on %.1f%% of the slots) over the same time" % (100.0 * narrow / max(slots, 1))},
+                             "over the kernel time; streamed_frac: the bytes this layout moves (values, then "
+                             "%.2f B of column per slot: 16-bit offsets on %.1f%% of the slots, lanes with equal "
+                             "column lists sharing one) over the same time"
+                             % (kinfo.col_stream_bytes / max(slots, 1), 100.0 * narrow / max(slots, 1))},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * nc,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms, 4),
                 "call_ms_min_median_max": [round(float(calls_ms.min()), 4), round(float(np.median(calls_ms)), 4),
@@ -758,7 +760,7 @@ def cg_one_gpu(args, a, n, nc, nnz, bd, dd, b, diag, kernel, row_order, local):
     slots, narrow = int(kinfo.stored_slots), int(kinfo.narrow_slots)
     b_it = 12 * nnz + 104 * n + (12 * nnz + 24 * n) / 50
     # the bytes the layout streams instead of 12 B/nnz (padding; 16-bit columns)
-    lay_bytes = 8 * slots + 2 * narrow + 4 * (slots - narrow)
+    lay_bytes = 8 * slots + int(kinfo.col_stream_bytes)
     s_it = b_it + (lay_bytes - 12 * nnz) * (1 + 1 / 50)
     # dominant kernel: the SpMV (~2/3 of an iteration), timed alone with CUDA
     # events on its stream, x (a CG direction) L2-resident as in the solve

@@ -113,6 +113,8 @@ typedef struct ew_layout_info {
     int64_t device_bytes; /* HBM held by the layout */
     int64_t narrow_slots; /* K1: slots whose columns stream as 16-bit offsets
                              from a per-warp base (0: all int32) */
+    int64_t col_stream_bytes; /* column bytes one SpMV launch streams (int32,
+                                 16-bit, or shared per lane group) */
 } ew_layout_info;
 
 /* Host views of a layout, in the reference's int64/double element types.
@@ -159,6 +161,7 @@ typedef struct ew_kernel_info {
     int32_t layout_kind;  /* 0 = csr_ref, else ew_layout_kind */
     int64_t device_bytes;
     int64_t narrow_slots; /* as ew_layout_info::narrow_slots */
+    int64_t col_stream_bytes; /* as ew_layout_info::col_stream_bytes */
 } ew_kernel_info;
 
 /* ---- errors / library ---------------------------------------------------- */

@@ -78,7 +78,8 @@ class LayoutInfo(C.Structure):
     _fields_ = [("kind", C.c_int32), ("warp_size", C.c_int32), ("row_major", C.c_int32),
                 ("sorted", C.c_int32), ("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("nwarps", C.c_int64), ("nslots", C.c_int64), ("stored_slots", C.c_int64),
-                ("threshold", C.c_int64), ("device_bytes", C.c_int64), ("narrow_slots", C.c_int64)]
+                ("threshold", C.c_int64), ("device_bytes", C.c_int64), ("narrow_slots", C.c_int64),
+                ("col_stream_bytes", C.c_int64)]
 
 
 class LayoutArrays(C.Structure):
@@ -99,7 +100,8 @@ class LayoutDesc(C.Structure):
 class KernelInfo(C.Structure):
     _fields_ = [("id", C.c_char * 16), ("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("stored_slots", C.c_int64), ("nwarps", C.c_int64), ("has_perm", C.c_int32),
-                ("layout_kind", C.c_int32), ("device_bytes", C.c_int64), ("narrow_slots", C.c_int64)]
+                ("layout_kind", C.c_int32), ("device_bytes", C.c_int64), ("narrow_slots", C.c_int64),
+                ("col_stream_bytes", C.c_int64)]
 
 
 OPERATOR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)

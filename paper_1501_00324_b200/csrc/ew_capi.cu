@@ -341,6 +341,7 @@ ew_status ew_layout_get_info(ew_layout l, ew_layout_info* info) {
         info->threshold = d.threshold;
         info->device_bytes = static_cast<int64_t>(d.device_bytes());
         info->narrow_slots = d.compact ? d.narrow_slots : 0;
+        info->col_stream_bytes = ew::layout_col_stream_bytes(d);
     });
 }
 
@@ -453,6 +454,7 @@ ew_status ew_kernel_get_info(ew_kernel k, ew_kernel_info* info) {
             d.layout ? d.layout->device_bytes()
                      : d.csr->device_bytes() + (d.format ? d.format->device_bytes() : size_t{0}));
         info->narrow_slots = d.layout && d.layout->compact ? d.layout->narrow_slots : 0;
+        info->col_stream_bytes = d.layout ? ew::layout_col_stream_bytes(*d.layout) : 4 * d.nnz;
     });
 }
 

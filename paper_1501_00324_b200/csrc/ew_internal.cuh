@@ -176,12 +176,27 @@ struct LayoutData {
     int64_t narrow_slots = 0;  // slots outside the wide (int32) warps
     DevBuf<uint16_t> cols16;   // per slot: col - col_base[w], 0xFFFF = padding (column 0)
     DevBuf<int32_t> col_base;  // per warp
+    // Grouped columns (K1 over 64 MB, ws = 32): consecutive lanes of a layout
+    // warp with identical column lists (the 3 unknowns of a node in a
+    // 3-DOF mesh) share one stored list; a lane reads its step-j column at
+    // gcols[goff[w] + j * ngrp[w] + lane_grp[p]] (16-bit offsets from
+    // col_base[w] when the layout is compact, else int32). The int32 / 16-bit
+    // slabs stay (export, refresh maps, the staged host pipeline).
+    int grouped = 0;
+    int64_t grouped_slots = 0;   // stored grouped column entries
+    int64_t grouped_col_bytes = 0;  // column bytes a grouped SpMV launch streams
+    DevBuf<uint8_t> lane_grp;    // per sorted row
+    DevBuf<uint8_t> ngrp;        // per warp
+    DevBuf<int64_t> goff;        // per warp
+    DevBuf<int32_t> gcols;       // int32 form
+    DevBuf<uint16_t> gcols16;    // compact form
     DevBuf<int64_t> slot_map;  // lazily built value_slot_map (export)
     DevBuf<int64_t> src_map;   // lazily built per-slot source entry (values-only refresh)
     size_t device_bytes() const {
         return values.bytes() + cols.bytes() + warp_offset.bytes() + maxrows.bytes() +
                rows_in_warp.bytes() + reduction.bytes() + rows_offset_warp.bytes() + fwd.bytes() +
-               inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes() + cols16.bytes() + col_base.bytes();
+               inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes() + cols16.bytes() + col_base.bytes() +
+               lane_grp.bytes() + ngrp.bytes() + goff.bytes() + gcols.bytes() + gcols16.bytes();
     }
 };
 
@@ -373,6 +388,12 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
 // list): the host-buffer pipeline runs a layout in stages this way.
 void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, const double* x, double* y,
                        cudaStream_t s);
+// Column bytes one SpMV launch of the layout streams (int32 / 16-bit / grouped).
+inline int64_t layout_col_stream_bytes(const LayoutData& l) {
+    if (l.grouped) return l.grouped_col_bytes;
+    if (l.compact) return 2 * l.narrow_slots + 4 * (l.nslots - l.narrow_slots);
+    return 4 * l.nslots;
+}
 // K1 with x split: columns [0, nown) from x, the rest from xg (scatter store).
 void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,
                        cudaStream_t s);

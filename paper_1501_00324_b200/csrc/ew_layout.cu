@@ -527,6 +527,113 @@ static void compact_layout(LayoutData& l, cudaStream_t s) {
     l.compact = 1;
 }
 
+// ---- grouped columns for K1 -------------------------------------------------
+// One thread per sorted row (a hardware warp = a layout warp, ws = 32): a lane
+// starts a group unless its column list (all maxrows steps, padding
+// included) equals the previous lane's. lane_grp = its group, ngrp per warp.
+__global__ void group_lanes_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                   const int32_t* __restrict__ maxrows, const int32_t* __restrict__ rows_in_warp,
+                                   int64_t nrows, int64_t nwarps, uint8_t* __restrict__ lane_grp,
+                                   uint8_t* __restrict__ ngrp, int64_t* __restrict__ gsize) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w = p >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nwarps) return;  // whole hardware warps exit together
+    const int32_t mx = maxrows[w], riw = rows_in_warp[w];
+    const int64_t off = woff[w];
+    bool start = lane == 0;
+    if (lane > 0 && lane < riw) {
+        bool same = true;
+        for (int32_t j = 0; j < mx && same; ++j) same = cols[off + int64_t(j) * 32 + lane] == cols[off + int64_t(j) * 32 + lane - 1];
+        start = !same;
+    }
+    const unsigned starts = __ballot_sync(0xffffffffu, start);
+    const int g = __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+    if (p < nrows) lane_grp[p] = static_cast<uint8_t>(g);
+    if (lane == 0) {
+        const int ng = __popc(starts);
+        ngrp[w] = static_cast<uint8_t>(ng);
+        gsize[w] = int64_t(mx) * ng;
+    }
+}
+
+// The leader lane of each group copies its column list into the grouped slab
+// (16-bit offsets from col_base when `base` is given, 0xFFFF = padding).
+__global__ void group_fill_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                  const int32_t* __restrict__ maxrows, const int32_t* __restrict__ rows_in_warp,
+                                  const int32_t* __restrict__ slen, int64_t nwarps, const uint8_t* __restrict__ lane_grp,
+                                  const uint8_t* __restrict__ ngrp, const int64_t* __restrict__ goff,
+                                  const int32_t* __restrict__ base, int32_t* __restrict__ g32,
+                                  uint16_t* __restrict__ g16) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t w = p >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nwarps) return;
+    const int32_t mx = maxrows[w], riw = rows_in_warp[w];
+    const int g = lane < riw ? lane_grp[p] : -1;
+    const int prev = __shfl_up_sync(0xffffffffu, g, 1);
+    if (lane >= riw || (lane > 0 && prev == g)) return;  // not a group leader
+    if (g16 && base[w] < 0) return;  // a wide warp of a compact layout reads its own int32 columns
+    const int64_t off = woff[w], go = goff[w];
+    const int ng = ngrp[w];
+    const int32_t len = slen[p];
+    for (int32_t j = 0; j < mx; ++j) {
+        const int32_t c = cols[off + int64_t(j) * 32 + lane];
+        const int64_t at = go + int64_t(j) * ng + g;
+        if (g16) g16[at] = j < len ? static_cast<uint16_t>(c - base[w]) : uint16_t(0xFFFF);
+        else g32[at] = c;
+    }
+}
+
+// Grouped columns for a K1 slab over 64 MB (int32 or compact layouts; a
+// compact layout's wide warps keep reading their int32 columns) when lanes
+// share enough lists: the slab's
+// column bytes drop to ngrp/32 (3-DOF elasticity: 11.3 groups per 32 lanes;
+// 12 -> 9.4 B/slot int32, 10 -> 8.7 with 16-bit offsets). EW_GROUPED=0: off.
+static void group_layout(LayoutData& l, cudaStream_t s) {
+    static const int mode = [] {
+        const char* e = std::getenv("EW_GROUPED");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (mode == 0 || l.kind != EW_LAYOUT_K1 || l.row_major || l.ws != 32 || !l.sorted || l.nwarps == 0) return;
+    if (mode == 1 && l.nslots * 12 <= (64ll << 20)) return;
+    const int64_t nw = l.nwarps;
+    DevBuf<uint8_t> lg(l.nrows), ng(nw);
+    Scratch<int64_t> gsize(nw, s);
+    group_lanes_kernel<<<grid_for(nw * 32), kBlock, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
+                                                            l.rows_in_warp.get(), l.nrows, nw, lg.get(), ng.get(),
+                                                            gsize.get());
+    launched("group_lanes_kernel");
+    DevBuf<int64_t> go(nw);
+    exclusive_scan_i64(gsize.get(), go.get(), nw, s);
+    const int64_t total = read_scalar(go.get() + nw - 1, s) + read_scalar(gsize.get() + nw - 1, s);
+    if (double(total) > 0.75 * double(l.nslots)) return;  // too few shared lists to pay
+    if (l.compact) l.gcols16.alloc(total);
+    else l.gcols.alloc(total);
+    group_fill_kernel<<<grid_for(nw * 32), kBlock, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
+                                                           l.rows_in_warp.get(), l.slen.get(), nw, lg.get(), ng.get(),
+                                                           go.get(), l.compact ? l.col_base.get() : nullptr,
+                                                           l.gcols.get(), l.gcols16.get());
+    launched("group_fill_kernel");
+    int64_t bytes = 4 * total;
+    if (l.compact) {  // narrow warps stream 2 B per grouped entry, wide ones their own int32 slab
+        std::vector<int64_t> gs(nw), wo(nw);
+        std::vector<int32_t> b(nw), mxs(nw);
+        EW_CUDA_CHECK(cudaMemcpyAsync(gs.data(), gsize.get(), nw * 8, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaMemcpyAsync(b.data(), l.col_base.get(), nw * 4, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaMemcpyAsync(mxs.data(), l.maxrows.get(), nw * 4, cudaMemcpyDeviceToHost, s));
+        EW_CUDA_CHECK(cudaStreamSynchronize(s));
+        bytes = 0;
+        for (int64_t w = 0; w < nw; ++w) bytes += b[w] >= 0 ? 2 * gs[w] : 4 * int64_t(mxs[w]) * l.ws;
+    }
+    l.lane_grp = std::move(lg);
+    l.ngrp = std::move(ng);
+    l.goff = std::move(go);
+    l.grouped_slots = total;
+    l.grouped_col_bytes = bytes;
+    l.grouped = 1;
+}
+
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s) {
@@ -658,7 +765,10 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
                                                   l.cols.get());
         launched("fill_kernel");
     }
-    if (kind == EW_LAYOUT_K1 && !l.row_major && nw) compact_layout(l, s);
+    if (kind == EW_LAYOUT_K1 && !l.row_major && nw) {
+        compact_layout(l, s);
+        group_layout(l, s);
+    }
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     return L;
 }

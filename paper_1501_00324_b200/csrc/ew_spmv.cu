@@ -74,6 +74,12 @@ struct K1Args {
     const int32_t* col_base;  // COMPACT: per-warp smallest column
     const int32_t* widx;      // INDIRECT: the layout warps to run, thread i -> warp widx[i / ws]
     int64_t nidx;             // INDIRECT: entries of widx
+    // GROUPED (LayoutData::grouped): shared column lists
+    const uint8_t* lane_grp;
+    const uint8_t* ngrp;
+    const int64_t* goff;
+    const int32_t* gcols;
+    const uint16_t* gcols16;
 };
 
 __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p, uint64_t pol) {
@@ -185,6 +191,93 @@ __device__ __forceinline__ double lane_sum_split(const double* __restrict__ vals
                       s, step, mx, pol);
 }
 
+// lane_sum_x with the columns read from a grouped list: step j's column at
+// gc(g + j * ng) (the values still at s + j * step). Same loads in flight,
+// same order of the adds.
+template <typename ColLoad, typename XLoad>
+__device__ __forceinline__ double lane_sum_gx(const double* __restrict__ vals, ColLoad gc, XLoad ld_x, int64_t s,
+                                              int64_t step, int64_t g, int32_t ng, int32_t mx, uint64_t pol) {
+    double sum = 0.0;
+    int32_t j = 0;
+    for (; j + 8 <= mx; j += 8) {
+        int32_t c[8];
+        double v[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = gc(g + u * ng, pol);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = ld_x(c[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum = madd(sum, v[u], xv[u]);
+        s += 8 * step;
+        g += 8 * ng;
+    }
+    if (j + 4 <= mx) {
+        int32_t c[4];
+        double v[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = gc(g + u * ng, pol);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = ld_x(c[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sum = madd(sum, v[u], xv[u]);
+        s += 4 * step;
+        g += 4 * ng;
+        j += 4;
+    }
+    const int32_t rem = mx - j;
+    if (rem > 0) {
+        int32_t c[3];
+        double v[3], xv[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) c[u] = gc(g + u * ng, pol);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) v[u] = ld_stream(vals + s + u * step, pol);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) xv[u] = ld_x(c[u]);
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+            if (u < rem) sum = madd(sum, v[u], xv[u]);
+    }
+    return sum;
+}
+
+// One K1 lane sum of sorted row p (layout warp w) from the grouped column
+// lists: 16-bit offsets when the layout is compact (its wide warps read their
+// own int32 columns), else int32. x gathers with the evict_last hint.
+template <bool COMPACT>
+__device__ __forceinline__ double k1_row_grouped(const K1Args& a, int64_t w, int64_t p, int64_t s, int32_t mx,
+                                                 uint64_t pol) {
+    const int64_t g = a.goff[w] + a.lane_grp[p];
+    const int32_t ng = a.ngrp[w];
+    const double* x = a.x;
+    uint64_t keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    auto ldx = [x, keep](int32_t c) {
+        double v;
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(x + c), "l"(keep));
+        return v;
+    };
+    if (COMPACT) {
+        const int32_t base = a.col_base[w];
+        if (base < 0) return lane_sum(a.values, a.cols, a.x, s, a.ws, mx, pol);  // a wide warp: own int32 columns
+        const uint16_t* g16 = a.gcols16;
+        return lane_sum_gx(a.values, [g16, base](int64_t i, uint64_t pl) {
+            const uint16_t d = ld_stream(g16 + i, pl);
+            return d == 0xFFFFu ? 0 : base + static_cast<int32_t>(d);
+        }, ldx, s, a.ws, g, ng, mx, pol);
+    }
+    const int32_t* g32 = a.gcols;
+    return lane_sum_gx(a.values, [g32](int64_t i, uint64_t pl) { return ld_stream(g32 + i, pl); }, ldx, s, a.ws, g,
+                       ng, mx, pol);
+}
+
 // One K1 lane sum of layout warp w. COMPACT: 16-bit columns (LayoutData::
 // cols16: 10 instead of 12 bytes per slot streamed) for the warps that have
 // them; x gathers with the evict_last hint either way.
@@ -219,7 +312,7 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
 // pipeline's stages, ew_kernel.cu): the same warps, lanes and padding as the
 // whole-layout launch, so the same row sums.
 template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool COMPACT = false,
-          bool INDIRECT = false>
+          bool INDIRECT = false, bool GROUPED = false>
 __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_kernel(K1Args a) {
     pdl_wait();
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -239,8 +332,11 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_k
         const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
         const int32_t mx = a.maxrows[w];
         const int64_t s = a.woff[w] + (ROW_MAJOR ? int64_t(lane) * mx : lane);
-        sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, ROW_MAJOR ? 1 : a.ws, mx, pol)
-                      : k1_row<COMPACT>(a, w, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
+        if (GROUPED)
+            sum = k1_row_grouped<COMPACT>(a, w, p, s, mx, pol);
+        else
+            sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, ROW_MAJOR ? 1 : a.ws, mx, pol)
+                          : k1_row<COMPACT>(a, w, s, ROW_MAJOR ? 1 : a.ws, mx, pol);
     }
     a.y[target] = sum;
     pdl_trigger();
@@ -260,7 +356,7 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_k
 // bit-identical results. Layouts with 16-bit columns (compact_layout) run the
 // plain form instead: with the narrower column loads the stream form spills
 // more (221 us cold on config 2) and the plain one wins (158.0 us vs 163.6).
-template <bool SORTED, bool SCATTER, bool SPLIT_X = false>
+template <bool SORTED, bool SCATTER, bool SPLIT_X = false, bool GROUPED = false>
 __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
     pdl_wait();
     if (a.done && *a.done) return;
@@ -274,8 +370,11 @@ __global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
             const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
             const int32_t mx = a.maxrows[w];
             const int64_t s = a.woff[w] + lane;
-            sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, a.ws, mx, pol)
-                          : lane_sum_ldg(a.values, a.cols, a.x, s, a.ws, mx, pol);
+            if (GROUPED)
+                sum = k1_row_grouped<false>(a, w, p, s, mx, pol);
+            else
+                sum = SPLIT_X ? lane_sum_split(a.values, a.cols, a.x, a.xg, a.nown, s, a.ws, mx, pol)
+                              : lane_sum_ldg(a.values, a.cols, a.x, s, a.ws, mx, pol);
         }
         a.y[SCATTER ? a.fwd[p] : p] = sum;
     }
@@ -558,7 +657,7 @@ inline bool streams(const LayoutData& l) {
 // each row adds x[target] * y[target] to its CTA's fixed-order partial;
 // cg::dot_final_kernel sums the partials and decides. The CTA only stores
 // its partial: no fence or atomic holds it past its last row.
-template <bool SORTED, bool SCATTER, bool COMPACT = false>
+template <bool SORTED, bool SCATTER, bool COMPACT = false, bool GROUPED = false>
 __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
@@ -574,7 +673,8 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_d
         if (active) {
             const int64_t w = p >> a.ws_log2;
             const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
-            sum = k1_row<COMPACT>(a, w, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+            sum = GROUPED ? k1_row_grouped<COMPACT>(a, w, p, a.woff[w] + lane, a.maxrows[w], pol)
+                          : k1_row<COMPACT>(a, w, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
         }
         a.y[t] = sum;
         v[0] = __dmul_rn(xt, sum);
@@ -587,7 +687,7 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_d
 }
 
 // k1_dot_kernel in the grid-stride form of k1_stream_kernel (large long-row layouts).
-template <bool SORTED, bool SCATTER>
+template <bool SORTED, bool SCATTER, bool GROUPED = false>
 __global__ void __launch_bounds__(256, 8) k1_dot_stream_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
@@ -600,7 +700,8 @@ __global__ void __launch_bounds__(256, 8) k1_dot_stream_kernel(K1Args a, double*
         if (active) {
             const int64_t w = p >> a.ws_log2;
             const int32_t lane = static_cast<int32_t>(p & (a.ws - 1));
-            sum = lane_sum_ldg(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
+            sum = GROUPED ? k1_row_grouped<false>(a, w, p, a.woff[w] + lane, a.maxrows[w], pol)
+                          : lane_sum_ldg(a.values, a.cols, a.x, a.woff[w] + lane, a.ws, a.maxrows[w], pol);
         }
         const int64_t t = SCATTER ? a.fwd[p] : p;
         a.y[t] = sum;
@@ -732,6 +833,22 @@ void launch_k1(const K1Args& a, bool row_major, bool stream_form, bool compact, 
     launched("k1_kernel");
 }
 
+template <bool SCATTER>
+void launch_k1_grouped(const K1Args& a, bool stream_form, bool compact, cudaStream_t s) {
+    if (compact) {
+        static const int cb = [] {
+            const char* e = std::getenv("EW_K1C_BLOCK");
+            return cta_size_knob(e, 64);
+        }();
+        launch_pdl(k1_kernel<true, SCATTER, false, false, true, false, true>, grid_for(a.nrows, cb), cb, s, a);
+    } else if (stream_form) {
+        launch_pdl(k1_stream_kernel<true, SCATTER, false, true>, grid_for(a.nrows), kBlock, s, a);
+    } else {
+        launch_pdl(k1_kernel<true, SCATTER, false, false, false, false, true>, grid_for(a.nrows), kBlock, s, a);
+    }
+    launched("k1_kernel");
+}
+
 template <bool SORTED, bool SCATTER>
 void launch_k2(const K2Args& a, cudaStream_t s) {
     if (a.nwarps == 0) return;
@@ -772,7 +889,8 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     if (l.kind != EW_LAYOUT_K1) return false;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
-             l.cols16.get(), l.col_base.get()};
+             l.cols16.get(), l.col_base.get(), nullptr, 0, l.lane_grp.get(), l.ngrp.get(), l.goff.get(),
+             l.gcols.get(), l.gcols16.get()};
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
     const bool c = l.compact != 0;
@@ -785,7 +903,14 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
     const int block = c ? cb : 256;
     const unsigned g = grid_for(l.nrows, block);
     auto go = [&](auto kernel) { launch_pdl(kernel, g, block, s, a, sink.partials); };
-    if (c) {
+    if (l.grouped) {  // sorted by construction
+        if (c)
+            scatter ? go(k1_dot_kernel<true, true, true, true>) : go(k1_dot_kernel<true, false, true, true>);
+        else if (streams(l))
+            scatter ? go(k1_dot_stream_kernel<true, true, true>) : go(k1_dot_stream_kernel<true, false, true>);
+        else
+            scatter ? go(k1_dot_kernel<true, true, false, true>) : go(k1_dot_kernel<true, false, false, true>);
+    } else if (c) {
         if (l.sorted)
             scatter ? go(k1_dot_kernel<true, true, true>) : go(k1_dot_kernel<true, false, true>);
         else
@@ -815,7 +940,8 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
     if (l.kind == EW_LAYOUT_K1) {
         K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
                  l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
-             l.cols16.get(), l.col_base.get()};
+                 l.cols16.get(), l.col_base.get(), nullptr, 0, l.lane_grp.get(), l.ngrp.get(), l.goff.get(),
+                 l.gcols.get(), l.gcols16.get()};
         const bool rm = l.row_major != 0, sf = streams(l), c = l.compact != 0;
         if (const int h = coop_warps(l)) {
             // EW_K1_BULK=1: the bulk-copy staging form (A/B; needs the
@@ -828,6 +954,10 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                 scatter ? launch_k1_bulk<true>(a, l.nwarps, h, s) : launch_k1_bulk<false>(a, l.nwarps, h, s);
             else
                 scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
+            return;
+        }
+        if (l.grouped) {  // sorted, column-major by construction
+            scatter ? launch_k1_grouped<true>(a, sf, c, s) : launch_k1_grouped<false>(a, sf, c, s);
             return;
         }
         if (l.sorted) {
