@@ -1,5 +1,7 @@
 // Device CSR: upload + validate_csr, the csr_ref SpMV, extract_diagonal,
 // permutation gather/scatter.
+#include <cuda.h>
+
 #include "ew_internal.cuh"
 
 namespace ew {
@@ -21,6 +23,54 @@ void retain_pool() {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     done_mask.fetch_or(bit, std::memory_order_relaxed);
+}
+
+void load_all_kernels() {
+    static std::mutex mu;
+    static uint64_t done_mask = 0;  // one bit per device ordinal (< 64)
+    int dev = 0;
+    EW_CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = dev < 64 ? uint64_t{1} << dev : 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done_mask & bit) return;
+    // each translation unit is one library; loading one kernel of it by
+    // handle (cuKernelGetFunction) loads it into the current context
+    using GetLibrary = CUresult (*)(CUlibrary*, CUkernel);
+    using KernelCount = CUresult (*)(unsigned*, CUlibrary);
+    using Enumerate = CUresult (*)(CUkernel*, unsigned, CUlibrary);
+    using GetFunction = CUresult (*)(CUfunction*, CUkernel);
+    auto entry = [](const char* name) -> void* {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion(name, &p, 12050, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return p;
+    };
+    auto get_library = reinterpret_cast<GetLibrary>(entry("cuKernelGetLibrary"));
+    auto kernel_count = reinterpret_cast<KernelCount>(entry("cuLibraryGetKernelCount"));
+    auto enumerate = reinterpret_cast<Enumerate>(entry("cuLibraryEnumerateKernels"));
+    auto get_function = reinterpret_cast<GetFunction>(entry("cuKernelGetFunction"));
+    require(get_library && kernel_count && enumerate && get_function,
+            "load_all_kernels: the driver lacks cuLibraryEnumerateKernels (CUDA >= 12.5)");
+    for (const void* anchor : {kernel_anchor_assembly(), kernel_anchor_dist(), kernel_anchor_formats(),
+                               kernel_anchor_kernel(), kernel_anchor_layout(), kernel_anchor_order(),
+                               kernel_anchor_spmv(), kernel_anchor_csr()}) {
+        cudaKernel_t k = nullptr;
+        EW_CUDA_CHECK(cudaGetKernel(&k, anchor));
+        CUlibrary lib = nullptr;
+        unsigned n = 0;
+        require(get_library(&lib, reinterpret_cast<CUkernel>(k)) == CUDA_SUCCESS &&
+                    kernel_count(&n, lib) == CUDA_SUCCESS,
+                "load_all_kernels: cannot enumerate a kernel library");
+        std::vector<CUkernel> all(n);
+        require(n == 0 || enumerate(all.data(), n, lib) == CUDA_SUCCESS, "load_all_kernels: enumeration failed");
+        for (CUkernel kk : all) {
+            CUfunction fn = nullptr;
+            require(get_function(&fn, kk) == CUDA_SUCCESS, "load_all_kernels: cannot load a kernel");
+        }
+    }
+    done_mask |= bit;
 }
 
 namespace {
@@ -195,5 +245,7 @@ void scatter(const int32_t* idx, const double* in, double* out, int64_t n, cudaS
     scatter_kernel<<<grid_for(n), kBlock, 0, s>>>(idx, in, out, n);
     launched("scatter_kernel");
 }
+
+const void* kernel_anchor_csr() { return reinterpret_cast<const void*>(&validate_rows_kernel); }
 
 }  // namespace ew

@@ -580,6 +580,7 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
                 const int64_t* bci, const double* bv, const std::vector<int64_t>& ghosts,
                 const std::vector<std::vector<int64_t>>& peer_needs, const std::string& kid,
                 const ew_warp_config& cfg, const ew_kernel_options& opts, cudaStream_t s) {
+    load_all_kernels();  // before any exchange: no lazy load while a peer spins
     P.part = g;
     P.r0 = bounds[g];
     P.r1 = bounds[g + 1];
@@ -1618,5 +1619,7 @@ void nccl_unique_id(void* out) {
     nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
     std::memcpy(out, &id, sizeof(id));
 }
+
+const void* kernel_anchor_dist() { return reinterpret_cast<const void*>(&pack_kernel); }
 
 }  // namespace ew

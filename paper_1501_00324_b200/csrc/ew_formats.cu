@@ -333,4 +333,6 @@ void format_spmv(const FormatData& f, const CsrData& m, const double* x, double*
     }
 }
 
+const void* kernel_anchor_formats() { return reinterpret_cast<const void*>(&ell_build_kernel); }
+
 }  // namespace ew

@@ -114,6 +114,22 @@ class DevBuf {
 // ~0.1 ms).
 void retain_pool();
 
+// Loads every kernel of this library into the current device's context now.
+// Under CUDA's default lazy loading a kernel's first launch loads it, and a
+// load can wait for the device: a partition loading its SpMV or push kernel
+// while a peer's kernel spins waiting for it deadlocks (seen with two
+// partitions on one GPU). Every partitioned operator calls this before its
+// first exchange. Once per device.
+void load_all_kernels();
+const void* kernel_anchor_assembly();
+const void* kernel_anchor_dist();
+const void* kernel_anchor_formats();
+const void* kernel_anchor_kernel();
+const void* kernel_anchor_layout();
+const void* kernel_anchor_order();
+const void* kernel_anchor_spmv();
+const void* kernel_anchor_csr();
+
 // Stream-ordered scratch (cudaMallocAsync from the device's default pool).
 template <typename T>
 class Scratch {

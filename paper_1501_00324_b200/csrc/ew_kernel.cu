@@ -288,4 +288,6 @@ bool kernel_apply_host(const KernelData& k, const double* x, double* y, cudaStre
     return true;
 }
 
+const void* kernel_anchor_kernel() { return reinterpret_cast<const void*>(&row_maxcol_kernel); }
+
 }  // namespace ew

@@ -924,4 +924,6 @@ std::shared_ptr<LayoutData> import_layout(const ew_layout_desc& d, cudaStream_t 
     return L;
 }
 
+const void* kernel_anchor_layout() { return reinterpret_cast<const void*>(&sort_keys_kernel); }
+
 }  // namespace ew

@@ -272,4 +272,6 @@ std::shared_ptr<CsrData> locality_operand(const CsrData& m, const CsrData& op, c
     return out;
 }
 
+const void* kernel_anchor_order() { return reinterpret_cast<const void*>(&start_kernel); }
+
 }  // namespace ew

@@ -1016,4 +1016,6 @@ void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, i
     launched("k1_kernel");
 }
 
+const void* kernel_anchor_spmv() { return reinterpret_cast<const void*>(&k1_stream_kernel<true, false>); }
+
 }  // namespace ew
