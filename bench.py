@@ -668,6 +668,9 @@ def run_cg_dist(args, rank, world, local, shape="c2-slab"):
     nnz_all, n_all = sum_over_ranks([float(nnz), float(nloc)], world)
     b_it = 12 * nnz_all + 104 * n_all + (12 * nnz_all + 24 * n_all) / 50
     per_gpu = b_it / world * it_s / 1e9
+    # the same with the bytes the partition's layouts stream (padding, grouped columns)
+    (sb_all,) = sum_over_ranks([float(sum(d.info(i)["stream_bytes"] for i in range(1)))], world)
+    s_it = sb_all + 104 * n_all + (sb_all + 24 * n_all) / 50
     # end to end: host b / diag in, solution + history out, every rank
     bh, dh = b.cpu().numpy(), diag
     barrier(world)
@@ -697,13 +700,16 @@ def run_cg_dist(args, rank, world, local, shape="c2-slab"):
                    "step_ms_rank0": step_ms},
         "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1), "peak": hbm, "peak_source": peak_src,
                      "unit": "GB/s", "frac": round(per_gpu / hbm, 4),
+                     "streamed_frac": round(s_it / world * it_s / 1e9 / hbm, 4),
+                     "streamed_bytes_per_iteration": s_it,
                      "traffic": (ncu_traffic(f"c5/cg_k1_dot_strong/n{world}") if strong else ncu_traffic("c5/cg_k1_dot"))
                      if args.scale == 1.0 else None,
                      "traffic_source": "profiles/ncu_traffic.json: DRAM bytes per launch of the iteration's dominant "
                                        "kernel, the fused SpMV + p.q (one per iteration)",
                      "algorithmic_bytes_per_iteration": b_it,
-                     "note": "per-GPU share of 12 nnz + 104 n + refresh bytes per iteration / max-over-ranks "
-                             "iteration time"},
+                     "note": "frac: per-GPU share of 12 nnz + 104 n + refresh bytes per iteration / "
+                             "max-over-ranks iteration time; streamed_frac: the same with the partition layouts' "
+                             "own matrix bytes (padding, grouped columns) in place of 12 B/nnz"},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if strong and rank == 0 and world == 1 and not args.no_cpu_baseline:

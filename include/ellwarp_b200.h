@@ -359,6 +359,11 @@ ew_status ew_dist_destroy(ew_dist d);
 /* Row range, ghost count and send count of local partition i. */
 ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* row_begin, int64_t* row_end,
                            int64_t* nghost, int64_t* nsend);
+/* Matrix bytes of local partition i's layouts (interior + boundary, or the
+ * one local layout): stored slots, and the value + column bytes one SpMV
+ * streams (8 per slot + 4 / 2 / grouped column bytes; csr_ref: 12 nnz). */
+ew_status ew_dist_get_layout_bytes(ew_dist d, int32_t local_index, int64_t* stored_slots,
+                                   int64_t* stream_bytes);
 /* y = A x on this process's owned rows (concatenated in partition order). */
 ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, void* stream);
 /* cg_solve (cg.cpp:25-104) over the partitioned operator: halo exchange per

@@ -178,6 +178,7 @@ _SIGS = {
                                      _vp]),
     "ew_dist_destroy": (C.c_int, [_vp]),
     "ew_dist_get_info": (C.c_int, [_vp, C.c_int32, _i64p, _i64p, _i64p, _i64p]),
+    "ew_dist_get_layout_bytes": (C.c_int, [_vp, C.c_int32, _i64p, _i64p]),
     "ew_dist_spmv": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "ew_dist_cg_solve": (C.c_int, [_vp, _vp, _vp, C.POINTER(CgConfig), C.c_int, _vp, _vp, C.POINTER(CgResultC),
                                    _vp]),
@@ -827,7 +828,10 @@ class Dist:
     def info(self, i=0):
         r0, r1, ng, ns = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         check(lib().ew_dist_get_info(self.h, i, C.byref(r0), C.byref(r1), C.byref(ng), C.byref(ns)))
-        return dict(row_begin=r0.value, row_end=r1.value, nghost=ng.value, nsend=ns.value)
+        sl, sb = C.c_int64(), C.c_int64()
+        check(lib().ew_dist_get_layout_bytes(self.h, i, C.byref(sl), C.byref(sb)))
+        return dict(row_begin=r0.value, row_end=r1.value, nghost=ng.value, nsend=ns.value,
+                    stored_slots=sl.value, stream_bytes=sb.value)
 
     def spmv(self, x, y=None, stream=None):
         if hasattr(x, "data_ptr"):

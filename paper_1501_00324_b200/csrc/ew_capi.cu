@@ -772,6 +772,16 @@ ew_status ew_dist_get_info(ew_dist d, int32_t local_index, int64_t* r0, int64_t*
     });
 }
 
+ew_status ew_dist_get_layout_bytes(ew_dist d, int32_t local_index, int64_t* stored_slots, int64_t* stream_bytes) {
+    return guarded([&] {
+        check_handle(d, "dist");
+        int64_t a = 0, b = 0;
+        ew::dist_layout_bytes(*d->d, local_index, &a, &b);
+        if (stored_slots) *stored_slots = a;
+        if (stream_bytes) *stream_bytes = b;
+    });
+}
+
 ew_status ew_dist_spmv(ew_dist d, const double* x, double* y, ew_mem_kind mem, void* stream) {
     return guarded([&] {
         check_handle(d, "dist");

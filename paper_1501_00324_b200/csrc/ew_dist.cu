@@ -1189,6 +1189,17 @@ void dist_part_info(const DistData& D, int32_t i, int64_t* r0, int64_t* r1, int6
     *nsend = static_cast<int64_t>(P.send_idx.size());
 }
 
+void dist_layout_bytes(const DistData& D, int32_t i, int64_t* slots, int64_t* bytes) {
+    require(i >= 0 && i < static_cast<int32_t>(D.parts.size()), "no such local partition");
+    const DistPart& P = *D.parts[i];
+    *slots = *bytes = 0;
+    for (const KernelData* k : {P.op_int.get(), P.op_bnd.get(), D.split ? nullptr : P.op.get()}) {
+        if (!k) continue;
+        *slots += k->stored_slots;
+        *bytes += k->layout ? 8 * k->layout->nslots + layout_col_stream_bytes(*k->layout) : 12 * k->nnz;
+    }
+}
+
 // y = A x over this process's owned rows (device pointers, concatenated in
 // partition order).
 void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s) {

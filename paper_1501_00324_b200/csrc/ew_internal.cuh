@@ -501,6 +501,7 @@ std::shared_ptr<DistData> dist_create_block(int64_t nglobal, const int64_t* bro,
                                             const ew_kernel_options& opts, cudaStream_t s);
 int64_t dist_owned_rows(const DistData& D);
 void dist_part_info(const DistData& D, int32_t i, int64_t* r0, int64_t* r1, int64_t* nghost, int64_t* nsend);
+void dist_layout_bytes(const DistData& D, int32_t i, int64_t* slots, int64_t* bytes);
 void dist_spmv(DistData& D, const double* x, double* y, cudaStream_t s);
 // Throws if a peer-transport wait timed out (synchronises s).
 void dist_check_peers(const DistData& D, cudaStream_t s);

@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-2 captures after the grouped K1 column lists (one B200 under gpurun;
+# never a multi-rank command). Same recipe as capture_r02.sh.
+set -x
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum,l1tex__t_sector_hit_rate.pct,sm__warps_active.avg.pct_of_peak_sustained_active
+O=gpurun_out/prof
+mkdir -p $O
+# 1. K1 SpMV, config 2 (grouped 16-bit columns): 20 launches
+ncu --metrics $M --clock-control none -k regex:"k1_(stream_)?kernel" -s 5 -c 20 --csv --log-file $O/r02b_ncu_k1_c2_launches.csv \
+    python bench.py --steps 30 --warmup 3 --no-cpu-baseline --cg-steps 0 > /dev/null 2>&1
+# 2. partitioned CG on the whole config 5 (grouped int32 columns): 10 live iterations' kernels
+ncu --metrics $M --clock-control none -k regex:"k1_dot|dot_final|update_kernel|p_kernel|pq_kernel" -s 40 -c 40 --csv \
+    --log-file $O/r02b_ncu_cg_c5_launches.csv \
+    python bench.py --workload cg --config c5 --steps 1 --warmup 1 --iterations 50 --no-cpu-baseline > /dev/null 2>&1
+# 3. full sections of the grouped K1 on config 2
+ncu --set full --import-source on --clock-control none -k regex:"k1_(stream_)?kernel" -s 5 -c 1 -o $O/r02b_k1_c2_grouped_full \
+    python bench.py --steps 10 --warmup 3 --no-cpu-baseline --cg-steps 0 > /dev/null 2>&1
+ls -la $O

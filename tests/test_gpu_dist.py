@@ -262,6 +262,7 @@ def test_ipc_transport_two_processes(ew):
     for p in procs:
         p.join(timeout=60)
     for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
+        print("rank", rank, it)
         assert ok_spmv, (rank, it)
         assert ok_cg, (rank, it)
 
@@ -391,3 +392,23 @@ def test_reference_api_multi_gpu_cg(ew):
     assert two["iterations"] == one["iterations"]
     assert two["spmv_calls"] == one["spmv_calls"]
     assert np.allclose(two["solution"], 1.0, atol=1e-6)
+
+
+def test_dist_layout_bytes(ew):
+    """ew_dist_get_layout_bytes: one partition holds the single-GPU K1
+    layout (same slots, same streamed bytes); split partitions count their
+    interior and boundary layouts, every entry stored once."""
+    from oracle.oracle import Csr
+    from paper_1501_00324_b200 import workloads as W
+
+    n, _, ro, ci, v = W.elasticity_box(9, 8, 7)
+    m = Csr.make(n, n, ro, ci, v)
+    ki = ew.Kernel("k1", ew.Csr(n, n, ro, ci, v)).info()
+    one = ew.Dist.local(m, 1, transport="copy").info(0)
+    assert one["stored_slots"] == ki.stored_slots
+    assert one["stream_bytes"] == 8 * ki.stored_slots + ki.col_stream_bytes
+    d = ew.Dist.local(m, 3, transport="peer")
+    parts = [d.info(i) for i in range(3)]
+    assert sum(p["stored_slots"] for p in parts) >= m.nnz
+    for p in parts:
+        assert 10 * p["stored_slots"] <= p["stream_bytes"] <= 12 * p["stored_slots"]
