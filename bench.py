@@ -341,11 +341,14 @@ def dist_operator(args, rank, world, shape="c2-slab"):
 # ---------------------------------------------------------------------------
 def k1_label(k, info):
     """Which K1 kernel form layout_spmv launches for this layout (ew_spmv.cu)."""
-    if info.narrow_slots:
-        return "k1_kernel (16-bit columns on narrow warps, compact_layout)"
-    if info.stored_slots * 12 > 64 << 20 and info.stored_slots >= 24 * info.nrows:
-        return "k1_stream_kernel (grid-stride K1: layout beyond L2, >= 24 slots/row)"
-    return "k1_kernel"
+    slots, narrow = int(info.stored_slots), int(info.narrow_slots)
+    grouped = info.col_stream_bytes < 2 * narrow + 4 * (slots - narrow)  # lanes share column lists
+    g = ", grouped column lists" if grouped else ""
+    if narrow:
+        return f"k1_kernel (16-bit columns on narrow warps, compact_layout{g})"
+    if slots * 12 > 64 << 20 and slots >= 24 * info.nrows:
+        return f"k1_stream_kernel (grid-stride K1: layout beyond L2, >= 24 slots/row{g})"
+    return f"k1_kernel{' (' + g[2:] + ')' if g else ''}"
 
 
 def run_spmv(args, rank, world, local):
