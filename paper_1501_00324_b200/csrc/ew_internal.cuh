@@ -166,6 +166,28 @@ struct CsrData {
 
 // Device ELL-WARP layout (K1 or K2). Per-warp metadata is int32 except the
 // int64 slot offsets; columns and permutations are int32.
+// Row-length bound of the cooperative head of a sorted K1 layout whose
+// longest row exceeds 4x it (EW_K1_HEAD; 0 turns the split off).
+int32_t head_mx();
+
+// A second stream and fork / join events on the current device (RAII).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    SideStream() {
+        EW_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        EW_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        EW_CUDA_CHECK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    }
+    ~SideStream() {
+        if (join) cudaEventDestroy(join);
+        if (fork) cudaEventDestroy(fork);
+        if (s) cudaStreamDestroy(s);
+    }
+    SideStream(const SideStream&) = delete;
+    SideStream& operator=(const SideStream&) = delete;
+};
+
 struct LayoutData {
     int kind = EW_LAYOUT_K1;
     int ws = 32;
@@ -179,6 +201,11 @@ struct LayoutData {
     int64_t stored_slots = 0;
     int32_t max_reduction = 1;
     int32_t max_mx = 0;    // sorted K1: the longest warp's maxrows (0: unknown)
+    // Sorted K1 with a few very long rows (power-law matrices): the leading
+    // `head_warps` warps (rows over kHeadMx entries) run the cooperative K1
+    // on `side` while the plain K1 runs the rest (ew_spmv.cu, layout_spmv).
+    int64_t head_warps = 0;
+    std::shared_ptr<SideStream> side;
     bool imported = false;  // built elsewhere: K2 may not cover every row
     DevBuf<double> values;
     DevBuf<int32_t> cols;

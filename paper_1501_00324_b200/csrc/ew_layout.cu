@@ -634,6 +634,14 @@ static void group_layout(LayoutData& l, cudaStream_t s) {
     l.grouped = 1;
 }
 
+int32_t head_mx() {
+    static const int32_t v = [] {
+        const char* e = std::getenv("EW_K1_HEAD");  // 0: off; else the head's row-length bound
+        return e ? std::max(0, std::atoi(e)) : 64;
+    }();
+    return v;
+}
+
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s) {
@@ -746,6 +754,19 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
         l.nslots = last_off + int64_t(last_mx) * l.ws;
         // sorted longest-first: warp 0 holds the longest row
         if (kind == EW_LAYOUT_K1 && l.sorted) l.max_mx = read_scalar(l.maxrows.get(), s);
+        // a few very long rows: the warps over head_mx() entries (a prefix,
+        // maxrows falls with the warp index) go to the cooperative K1
+        const int32_t hm = head_mx();
+        if (kind == EW_LAYOUT_K1 && l.sorted && !row_major && l.ws == 32 && hm > 0 && l.max_mx > 4 * hm) {
+            int64_t lo = 0, hi = nw;  // first warp with maxrows <= hm
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) / 2;
+                if (read_scalar(l.maxrows.get() + mid, s) > hm) lo = mid + 1;
+                else hi = mid;
+            }
+            l.head_warps = lo;
+            if (lo > 0) l.side = std::make_shared<SideStream>();
+        }
     }
     sizes_owner.reset();
     unsigned long long hc[2];

@@ -80,6 +80,7 @@ struct K1Args {
     const int64_t* goff;
     const int32_t* gcols;
     const uint16_t* gcols16;
+    int64_t row_lo;  // k1_kernel (!INDIRECT): thread i runs sorted row row_lo + i (the tail of a head split)
 };
 
 __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p, uint64_t pol) {
@@ -316,6 +317,7 @@ template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool 
 __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_kernel(K1Args a) {
     pdl_wait();
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (!INDIRECT) p += a.row_lo;
     if (INDIRECT) {
         const int64_t i = p >> a.ws_log2;
         if (i >= a.nidx) return;
@@ -954,6 +956,31 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                 scatter ? launch_k1_bulk<true>(a, l.nwarps, h, s) : launch_k1_bulk<false>(a, l.nwarps, h, s);
             else
                 scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
+            return;
+        }
+        if (l.head_warps > 0 && !c && !l.grouped && !rm && !l.imported) {
+            // power-law rows, too many for the cooperative K1 everywhere
+            // (webbase: 1M rows, one of 4,700 entries): the head warps (rows
+            // over head_mx() entries) run the cooperative K1 on the side
+            // stream, the plain K1 the tail rows meanwhile; disjoint rows,
+            // the same row sums. Webbase 1,756 -> ~160 us; circuit keeps the
+            // cooperative K1 everywhere (773 vs 604 GB/s effective split)
+            const SideStream& ss = *l.side;
+            EW_CUDA_CHECK(cudaEventRecord(ss.fork, s));
+            EW_CUDA_CHECK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+            scatter ? launch_k1_coop<true>(a, l.head_warps, 8, false, ss.s)
+                    : launch_k1_coop<false>(a, l.head_warps, 8, false, ss.s);
+            const int64_t lo = l.head_warps * 32;
+            if (lo < l.nrows) {
+                K1Args t = a;
+                t.row_lo = lo;
+                const unsigned g = grid_for(l.nrows - lo);
+                scatter ? launch_pdl(k1_kernel<true, true, false>, g, kBlock, s, t)
+                        : launch_pdl(k1_kernel<true, false, false>, g, kBlock, s, t);
+                launched("k1_kernel");
+            }
+            EW_CUDA_CHECK(cudaEventRecord(ss.join, ss.s));
+            EW_CUDA_CHECK(cudaStreamWaitEvent(s, ss.join, 0));
             return;
         }
         if (l.grouped) {  // sorted, column-major by construction

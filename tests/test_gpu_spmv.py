@@ -334,3 +334,17 @@ def test_host_buffer_pipeline_nonfinite_x0(ew, R, F, shape):
     finally:
         R.free(lay)
     assert padded_rows > 0
+
+
+@pytest.mark.parametrize("kid", ["k1", "k1r", "k1rs"])
+def test_k1_head_split_power_law(ew, F, kid):
+    """A webbase-like matrix (120k rows, one row of 4,700 entries): the
+    warps of rows over 64 entries run the cooperative K1 on a side stream
+    while the plain K1 runs the rest -- bitwise the reference's K1."""
+    m = F.generate("powerlaw_rows:nrows=120000,alpha=1.2,maxrow=4700,seed=23")
+    x = F.random_vector(m.ncols, 7)
+    a = dev_csr(ew, m)
+    k = ew.Kernel(kid, a)
+    assert same(k.apply(x), F.apply(kid, m, x))
+    x[0] = np.nan  # padding terms 0 * x[0] as the reference executes them
+    assert same(k.apply(x), F.apply(kid, m, x))
