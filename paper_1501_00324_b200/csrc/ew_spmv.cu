@@ -855,7 +855,18 @@ template <bool SORTED, bool SCATTER>
 void launch_k2(const K2Args& a, cudaStream_t s) {
     if (a.nwarps == 0) return;
     if (a.ws <= 32) {
-        launch_pdl(k2_kernel<SORTED, SCATTER>, grid_for(a.nwarps * a.ws), kBlock, s, a, (double*)nullptr);
+        // 128-thread CTAs: the mid-size FEM layouts run ~1.05 waves of
+        // 256-thread CTAs at 6 per SM (accelerator: 935 CTAs, ncu 1.05
+        // waves, a third of the SM cycles idle); finer CTAs even the tail.
+        // Suite A/B on one box (cold us, 256 -> 128): accelerator 13.13 ->
+        // 12.43, economics 13.54 -> 12.22, protein 16.64 -> 15.72, ship
+        // 25.97 -> 24.80, circuit 10.91 -> 10.53; none slower (96 / 64 / 160
+        // within noise of 128 or worse)
+        static const int kb = [] {
+            const char* e = std::getenv("EW_K2_BLOCK");  // A/B runs: CTA size of the K2 SpMV
+            return cta_size_knob(e, 128);
+        }();
+        launch_pdl(k2_kernel<SORTED, SCATTER>, grid_for(a.nwarps * a.ws, kb), kb, s, a, (double*)nullptr);
     } else {
         k2_wide_kernel<SORTED, SCATTER><<<static_cast<unsigned>(a.nwarps), a.ws, a.ws * sizeof(double), s>>>(a);
     }
