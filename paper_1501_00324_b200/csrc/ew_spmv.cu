@@ -462,6 +462,93 @@ __global__ void __launch_bounds__(32 * H, H == 8 ? EW_COOP8_MINB : (H == 4 ? EW_
     pdl_trigger();
 }
 
+// K1 for the very long rows at the head of a power-law layout (the head of a
+// head split, layout_spmv): one 1024-thread CTA per layout warp. Warps 1-31
+// load and multiply 8 steps each of every chunk of 248 steps, warp 0 adds
+// the products in step order; two chunk buffers in shared memory change
+// hands through named barriers (FULL b: the producers arrive, the adder
+// waits; EMPTY b: the adder arrives, the producers wait before reusing b),
+// so the adds of chunk c overlap the loads of chunk c + 1. Same products,
+// same sequential sum per row as k1_kernel: bit-identical y.
+constexpr int kLongProducers = 31;
+constexpr int kLongChunk = 8 * kLongProducers;
+constexpr size_t kLongSmem = 2 * kLongChunk * 32 * sizeof(double);
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <bool SCATTER>
+__global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
+    extern __shared__ double prod[];  // [2][kLongChunk][32]
+    if (a.done && *a.done) return;    // uniform across the grid
+    const int64_t w = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t p = (w << 5) + lane;
+    const int32_t mx = __ldg(a.maxrows + w);
+    const int64_t wo = __ldg(a.woff + w);
+    const int nchunks = (mx + kLongChunk - 1) / kLongChunk;
+    if (warp == 0) {
+        const int64_t target = SCATTER && p < a.nrows ? a.fwd[p] : p;
+        double acc = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            named_sync(1 + b, 1024);  // chunk c is in buffer b
+            const double* buf = prod + b * (kLongChunk * 32);
+            const int n = min(kLongChunk, mx - c * kLongChunk);
+#pragma unroll 8
+            for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, buf[j * 32 + lane]);
+            if (c + 2 < nchunks) named_arrive(3 + b, 1024);  // buffer b free for chunk c + 2
+        }
+        if (p < a.nrows) a.y[target] = p < a.n_active ? acc : 0.0;
+    } else {
+        const uint64_t pol = evict_first_policy();
+        uint64_t keep;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+        const int q = warp - 1;
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            if (c >= 2) named_sync(3 + b, 1024);  // the adder is done with chunk c - 2
+            const int j0 = c * kLongChunk + q * 8;
+            const int cnt = min(8, mx - j0);
+            if (cnt > 0) {
+                const int64_t s0 = wo + int64_t(j0) * 32 + lane;
+                int32_t col[8];
+                double v[8], xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u < cnt) col[u] = ld_stream(a.cols + s0 + u * 32, pol);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u < cnt) v[u] = ld_stream(a.values + s0 + u * 32, pol);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u < cnt)
+                        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;"
+                                     : "=d"(xv[u])
+                                     : "l"(a.x + col[u]), "l"(keep));
+                double* buf = prod + b * (kLongChunk * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (u < cnt) buf[(q * 8 + u) * 32 + lane] = __dmul_rn(v[u], xv[u]);
+            }
+            named_arrive(1 + b, 1024);
+        }
+    }
+}
+
+template <bool SCATTER>
+void launch_k1_long(const K1Args& a, int64_t nwarps, cudaStream_t s) {
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kLongSmem)));
+    k1_long_kernel<SCATTER><<<static_cast<unsigned>(nwarps), 1024, kLongSmem, s>>>(a);
+    EW_CUDA_CHECK(cudaGetLastError());
+    launched("k1_long_kernel");
+}
+
 // ---- the same K1 with the warp's slab staged by the bulk-copy engine -------
 // k1_coop_kernel's loads (8 column + 8 value loads per lane and warp per
 // chunk, then the gathers) replaced by cp.async.bulk copies of whole chunks
@@ -974,13 +1061,23 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
             // (webbase: 1M rows, one of 4,700 entries): the head warps (rows
             // over head_mx() entries) run the cooperative K1 on the side
             // stream, the plain K1 the tail rows meanwhile; disjoint rows,
-            // the same row sums. Webbase 1,756 -> ~160 us; circuit keeps the
-            // cooperative K1 everywhere (773 vs 604 GB/s effective split)
+            // the same row sums. Webbase (cold): 1,756 us unsplit, ~160 us
+            // with k1_coop_kernel (H = 8) as the head, 76 us with
+            // k1_long_kernel (ncu: head 62 us, tail 39 us, concurrent);
+            // circuit keeps the cooperative K1 everywhere (773 vs 604 GB/s
+            // effective split)
             const SideStream& ss = *l.side;
             EW_CUDA_CHECK(cudaEventRecord(ss.fork, s));
             EW_CUDA_CHECK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
-            scatter ? launch_k1_coop<true>(a, l.head_warps, 8, false, ss.s)
-                    : launch_k1_coop<false>(a, l.head_warps, 8, false, ss.s);
+            static const bool coop_head = [] {  // A/B: the cooperative K1 (H = 8) for the head
+                const char* e = std::getenv("EW_K1_HEAD_COOP");
+                return e && e[0] == '1';
+            }();
+            if (coop_head)
+                scatter ? launch_k1_coop<true>(a, l.head_warps, 8, false, ss.s)
+                        : launch_k1_coop<false>(a, l.head_warps, 8, false, ss.s);
+            else
+                scatter ? launch_k1_long<true>(a, l.head_warps, ss.s) : launch_k1_long<false>(a, l.head_warps, ss.s);
             const int64_t lo = l.head_warps * 32;
             if (lo < l.nrows) {
                 K1Args t = a;
