@@ -169,6 +169,7 @@ struct CsrData {
 // Row-length bound of the cooperative head of a sorted K1 layout whose
 // longest row exceeds 4x it (EW_K1_HEAD; 0 turns the split off).
 int32_t head_mx();
+void k1_long_setup();  // ew_spmv.cu: k1_long_kernel's shared-memory opt-in (current device)
 
 // A second stream and fork / join events on the current device (RAII).
 struct SideStream {

@@ -765,7 +765,10 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
                 else hi = mid;
             }
             l.head_warps = lo;
-            if (lo > 0) l.side = std::make_shared<SideStream>();
+            if (lo > 0) {
+                l.side = std::make_shared<SideStream>();
+                k1_long_setup();
+            }
         }
     }
     sizes_owner.reset();

@@ -542,8 +542,6 @@ __global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
 
 template <bool SCATTER>
 void launch_k1_long(const K1Args& a, int64_t nwarps, cudaStream_t s) {
-    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kLongSmem)));
     k1_long_kernel<SCATTER><<<static_cast<unsigned>(nwarps), 1024, kLongSmem, s>>>(a);
     EW_CUDA_CHECK(cudaGetLastError());
     launched("k1_long_kernel");
@@ -1149,6 +1147,15 @@ void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, i
         launch_pdl(k1_kernel<false, true, false, true>, grid_for(a.nrows), kBlock, s, a);
     }
     launched("k1_kernel");
+}
+
+// Shared-memory opt-in of k1_long_kernel on the current device (a layout
+// with a head split calls this when it is built, outside any capture).
+void k1_long_setup() {
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kLongSmem)));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kLongSmem)));
 }
 
 const void* kernel_anchor_spmv() { return reinterpret_cast<const void*>(&k1_stream_kernel<true, false>); }
