@@ -1196,7 +1196,7 @@ void dist_layout_bytes(const DistData& D, int32_t i, int64_t* slots, int64_t* by
     for (const KernelData* k : {P.op_int.get(), P.op_bnd.get(), D.split ? nullptr : P.op.get()}) {
         if (!k) continue;
         *slots += k->stored_slots;
-        *bytes += k->layout ? 8 * k->layout->nslots + layout_col_stream_bytes(*k->layout) : 12 * k->nnz;
+        *bytes += k->layout ? 8 * k->layout->stored_slots + layout_col_stream_bytes(*k->layout) : 12 * k->nnz;
     }
 }
 

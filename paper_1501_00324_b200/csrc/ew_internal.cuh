@@ -433,10 +433,12 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
 void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, const double* x, double* y,
                        cudaStream_t s);
 // Column bytes one SpMV launch of the layout streams (int32 / 16-bit / grouped).
+// Counted over the stored slots (maxrows x ws per warp): the alignment gaps
+// between slabs are never read.
 inline int64_t layout_col_stream_bytes(const LayoutData& l) {
     if (l.grouped) return l.grouped_col_bytes;
-    if (l.compact) return 2 * l.narrow_slots + 4 * (l.nslots - l.narrow_slots);
-    return 4 * l.nslots;
+    if (l.compact) return 2 * l.narrow_slots + 4 * (l.stored_slots - l.narrow_slots);
+    return 4 * l.stored_slots;
 }
 // K1 with x split: columns [0, nown) from x, the rest from xg (scatter store).
 void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,

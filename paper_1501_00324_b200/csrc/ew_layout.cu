@@ -516,14 +516,14 @@ static void compact_layout(LayoutData& l, cudaStream_t s) {
         const char* e = std::getenv("EW_COMPACT_MIN");  // A/B runs: least narrow share
         return e ? std::atof(e) : 0.75;
     }();
-    if (double(l.nslots - wide) < min_narrow * double(l.nslots)) return;  // mostly wide warps
+    if (double(l.stored_slots - wide) < min_narrow * double(l.stored_slots)) return;  // mostly wide warps
     l.cols16.alloc(l.nslots);
     compact_encode_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
                                                               l.rows_in_warp.get(), l.slen.get(), l.ws, l.ws_log2,
                                                               l.nwarps, base.get(), l.cols16.get());
     launched("compact_encode_kernel");
     l.col_base = std::move(base);
-    l.narrow_slots = l.nslots - wide;
+    l.narrow_slots = l.stored_slots - wide;  // stored slots of the narrow warps
     l.compact = 1;
 }
 

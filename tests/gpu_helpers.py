@@ -1,6 +1,8 @@
 """Shared expectations for the GPU parity tests: what the reference computes
 for prepare_kernel(id).apply / apply_permuted (kernels.cpp:23-125), restated
 with the C oracle."""
+import contextlib
+
 import numpy as np
 
 
@@ -54,3 +56,40 @@ def same(a, b):
         return False
     na, nb = np.isnan(a), np.isnan(b)
     return bool(np.array_equal(na, nb) and np.array_equal(bits(a[~na]), bits(b[~nb])))
+
+
+@contextlib.contextmanager
+def mps_environment(tmpdir):
+    """A private CUDA MPS control daemon (pipe and log directories under
+    tmpdir) for test processes that must run CONCURRENTLY on one GPU: without
+    MPS, processes time-slice the GPU, and the peer transport's spin waits
+    (one rank's kernel waiting on another rank's store) then depend on the
+    slicing. Yields the environment for the child processes, or None when
+    MPS is unavailable (the callers then fall back to time-slicing). On one
+    GPU per process, the deployment layout, none of this applies."""
+    import os
+    import shutil
+    import subprocess
+
+    exe = shutil.which("nvidia-cuda-mps-control")
+    if not exe:
+        yield None
+        return
+    pipe, log = os.path.join(str(tmpdir), "mps_pipe"), os.path.join(str(tmpdir), "mps_log")
+    os.makedirs(pipe, exist_ok=True)
+    os.makedirs(log, exist_ok=True)
+    env = dict(os.environ, CUDA_MPS_PIPE_DIRECTORY=pipe, CUDA_MPS_LOG_DIRECTORY=log)
+    try:
+        started = subprocess.run([exe, "-d"], env=env, timeout=30, capture_output=True).returncode == 0
+    except (OSError, subprocess.SubprocessError):
+        started = False
+    if not started:
+        yield None
+        return
+    try:
+        yield env
+    finally:
+        try:
+            subprocess.run([exe], input="quit\n", text=True, env=env, timeout=60, capture_output=True)
+        except (OSError, subprocess.SubprocessError):
+            pass

@@ -244,33 +244,46 @@ def _ipc_worker(rank, world, port, q):
         q.put((rank, False, False, repr(e), None))
 
 
-def test_ipc_transport_two_processes(ew):
+def test_ipc_transport_two_processes(ew, tmp_path):
     """Two processes, one partition each, over the CUDA IPC peer transport
-    (gloo only for the setup allgather)."""
+    (gloo only for the setup allgather), run concurrently on this GPU under a
+    private MPS daemon when the image has one (else time-sliced, with the
+    worker's retries)."""
     import multiprocessing as mp
     import socket
+
+    from tests.gpu_helpers import mps_environment
 
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    out = [q.get(timeout=600) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
+    with mps_environment(tmp_path) as env:
+        saved = dict(os.environ)
+        if env:  # spawned children take the environment at start
+            os.environ.update(env)
+        try:
+            procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+            for p in procs:
+                p.start()
+        finally:
+            os.environ.clear()
+            os.environ.update(saved)
+        out = [q.get(timeout=600) for _ in procs]
+        for p in procs:
+            p.join(timeout=60)
     for rank, ok_spmv, ok_cg, it, ref_it in sorted(out, key=lambda t: t[0]):
-        print("rank", rank, it)
+        print("rank", rank, "mps" if env else "time-sliced", it)
         assert ok_spmv, (rank, it)
         assert ok_cg, (rank, it)
 
 
 def test_bench_two_ranks_functional(tmp_path):
     """bench.py's N > 1 path (partitioned SpMV + CG, IPC transport) under
-    torchrun with two ranks sharing this GPU: runs end to end and prints one
-    JSON line with both metrics (a functional check, not a measurement)."""
+    torchrun with two ranks sharing this GPU (concurrently under a private
+    MPS daemon when available): runs end to end and prints one JSON line with
+    both metrics (a functional check, not a measurement)."""
     import json
     import socket
     import subprocess
@@ -284,11 +297,14 @@ def test_bench_two_ranks_functional(tmp_path):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    env = dict(os.environ, EW_BENCH_SHARE_GPU="1")
+    from tests.gpu_helpers import mps_environment
+
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3",
            "--scale", "0.25", "--iterations", "60", "--cg-steps", "1", "--no-cpu-baseline"]
-    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    with mps_environment(tmp_path) as mps:
+        env = dict(mps or os.environ, EW_BENCH_SHARE_GPU="1")
+        out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["transport"] == "ipc"
