@@ -340,14 +340,9 @@ __global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* 
                                                            const double* __restrict__ diag, int64_t n, int jacobi,
                                                            double tol, double divergence,
                                                            double* partials, State* st, double* hist) {
-    pdl_wait();
-    if (st->done) return;
-    const double alpha = st->alpha;
     const uint64_t first = l2_policy_first(), last = l2_policy_last();
-    double v[2] = {0.0, 0.0};
-    int bad = 0;
-    EW_ROUNDS_U(i0, S, n, kUpdU) {
-        double xv[kUpdU], pv[kUpdU], qv[kUpdU], rv[kUpdU], dv[kUpdU];
+    double xv[kUpdU], pv[kUpdU], qv[kUpdU], rv[kUpdU], dv[kUpdU];
+    auto load = [&](int64_t i0, int64_t S) {
 #pragma unroll
         for (int u = 0; u < kUpdU; ++u) {
             const int64_t i = i0 + u * S;
@@ -358,6 +353,24 @@ __global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* 
             rv[u] = ok && mode != 1 ? (mode == 0 ? r[i] : b[i]) : 0.0;
             dv[u] = ok && mode != 1 && jacobi ? ld_hint(diag + i, last) : 1.0;
         }
+    };
+    // mode 0: the first round's loads go out before the wait for alpha and
+    // overlap the p.q reduction's tail. Safe: x, p, r, diag are older, and q
+    // comes from the SpMV, which the kernel before this one (dot_final or
+    // pq_kernel, triggering only after its own wait; or a plain launch)
+    // saw complete before this grid could start. Mode 2 reads a q that the
+    // SpMV right before it is still writing: no early loads.
+    const int64_t S0 = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool have = mode == 0 && t0 < n;
+    if (have) load(t0, S0);
+    pdl_wait();
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double v[2] = {0.0, 0.0};
+    int bad = 0;
+    EW_ROUNDS_U(i0, S, n, kUpdU) {
+        if (!have) load(i0, S);
+        have = false;
 #pragma unroll
         for (int u = 0; u < kUpdU; ++u) {
             const int64_t i = i0 + u * S;
@@ -388,19 +401,34 @@ __global__ void __launch_bounds__(kRedBlock, 4) update_kernel(int mode, double* 
 static __global__ void __launch_bounds__(256) p_kernel(double* __restrict__ p, const double* __restrict__ r,
                                                 const double* __restrict__ diag, int64_t n, int jacobi,
                                                 const State* st) {
+    double rv[kU], dv[kU], pv[kU];
+    // the first round's diag and p (neither is written by the update
+    // kernel this grid follows) go out before the wait; r after it
+    const int64_t S0 = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool have = t0 < n;
+    if (have) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = n - 1 - (t0 + u * S0);
+            dv[u] = i >= 0 && jacobi ? diag[i] : 1.0;
+            pv[u] = i >= 0 ? p[i] : 0.0;
+        }
+    }
     pdl_wait();
     if (st->done) return;
     const double beta = st->beta;
     EW_ROUNDS(i0, S, n) {
-        double rv[kU], dv[kU], pv[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int64_t i = n - 1 - (i0 + u * S);
             const bool ok = i >= 0;
             rv[u] = ok ? r[i] : 0.0;
-            dv[u] = ok && jacobi ? diag[i] : 1.0;
-            pv[u] = ok ? p[i] : 0.0;
+            if (!have) {
+                dv[u] = ok && jacobi ? diag[i] : 1.0;
+                pv[u] = ok ? p[i] : 0.0;
+            }
         }
+        have = false;
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int64_t i = n - 1 - (i0 + u * S);
@@ -421,6 +449,9 @@ static __global__ void __launch_bounds__(kRedBlock) dot_final_kernel(const doubl
                                                                      double* scratch, unsigned* tickets, State* st,
                                                                      int dist, int slot) {
     pdl_wait();
+    // the update kernel may launch now: it loads its first vectors while
+    // this grid sums (it reads alpha only after its own wait)
+    pdl_trigger();
     if (st->done) return;  // uniform across the grid
     const unsigned i = blockIdx.x * kRedBlock + threadIdx.x;
     double v[1] = {i < n ? part[i] : 0.0};
