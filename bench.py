@@ -480,6 +480,7 @@ def run_spmv(args, rank, world, local):
         "data": "synthetic (seeded structured tet mesh, values from P1 elasticity element matrices)",
         "config": {"workload": CONFIGS[args.config]["name"], "config": args.config, "kernel": args.kernel,
                    "permuted": bool(args.permuted), "nrows": n, "nnz": nnz, "stored_slots": k.stored_slots,
+                   "kernel_device_bytes": int(kinfo.device_bytes),
                    "per_rank": "independent copy per GPU" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (%.2f GB algorithmic bytes vs 126 MB L2)" % (alg_bytes / 1e9)
                    if alg_bytes > 3 * 126e6 else "L2-resident working set: warm-L2 number"},

@@ -352,7 +352,14 @@ ew_status ew_layout_export(ew_layout l, const ew_layout_arrays* out) {
         const auto& d = *l->d;
         if (out->values && d.nslots)
             EW_CUDA_CHECK(cudaMemcpy(out->values, d.values.get(), d.nslots * 8, cudaMemcpyDeviceToHost));
-        widen(d.cols, out->col_indices, d.nslots);
+        if (d.cols_full) {
+            widen(d.cols, out->col_indices, d.nslots);
+        } else if (out->col_indices && d.nslots) {  // dropped int32 slab: decode the kernels' forms
+            ew::DevBuf<int32_t> full(d.nslots);
+            ew::decode_columns(d, full.get(), nullptr);
+            EW_CUDA_CHECK(cudaStreamSynchronize(nullptr));
+            widen(full, out->col_indices, d.nslots);
+        }
         if (out->warp_offset && d.nwarps)
             EW_CUDA_CHECK(cudaMemcpy(out->warp_offset, d.warp_offset.get(), d.nwarps * 8,
                                      cudaMemcpyDeviceToHost));

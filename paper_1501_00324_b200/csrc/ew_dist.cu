@@ -609,6 +609,8 @@ void build_part(DistPart& P, int32_t g, int32_t G, const std::vector<int64_t>& b
         has_ghost.release();
         P.op_int = prepare_rows(*local, rows_int, P.n_int, kid, cfg, opts, s);
         P.op_bnd = prepare_rows(*local, rows_bnd, P.n_bnd, kid, cfg, opts, s);
+        // the boundary rows run the split-x K1, which reads the int32 slab
+        if (P.op_bnd->layout) restore_columns(*P.op_bnd->layout, s);
     } else {
         has_ghost.release();
         P.op = prepare(kid, *local, cfg, opts, s);

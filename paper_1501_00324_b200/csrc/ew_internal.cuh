@@ -169,6 +169,16 @@ struct CsrData {
 // Row-length bound of the cooperative head of a sorted K1 layout whose
 // longest row exceeds 4x it (EW_K1_HEAD; 0 turns the split off).
 int32_t head_mx();
+struct LayoutData;
+// The int32 column of every slot (nslots entries, alignment gaps 0) into
+// out, from whatever form the layout holds (ew_layout.cu).
+void decode_columns(const LayoutData& l, int32_t* out, cudaStream_t s);
+// Gives a shrunk layout its full int32 slab back (the split-x boundary K1 of
+// a partition reads it).
+void restore_columns(LayoutData& l, cudaStream_t s);
+// Whether layout_spmv / layout_spmv_dot read the full int32 slab for this
+// layout (ew_spmv.cu).
+bool spmv_reads_int32(const LayoutData& l);
 void k1_long_setup();  // ew_spmv.cu: k1_long_kernel's shared-memory opt-in (current device)
 
 // A second stream and fork / join events on the current device (RAII).
@@ -209,7 +219,14 @@ struct LayoutData {
     std::shared_ptr<SideStream> side;
     bool imported = false;  // built elsewhere: K2 may not cover every row
     DevBuf<double> values;
+    // int32 columns per slot. After shrink_columns (compact or grouped
+    // layouts, whose kernels read the 16-bit / grouped forms) only the wide
+    // warps' columns stay, slot s of wide warp w at cols[col_shift[w] + s]
+    // (col_shift empty and cols empty: a grouped int32 layout); cols_full
+    // false then, and decode_columns rebuilds the whole slab on demand.
     DevBuf<int32_t> cols;
+    DevBuf<int64_t> col_shift;
+    bool cols_full = true;
     DevBuf<int64_t> warp_offset;
     DevBuf<int32_t> maxrows, rows_in_warp, reduction, rows_offset_warp;
     DevBuf<int32_t> fwd, inv, slen;
@@ -240,7 +257,8 @@ struct LayoutData {
         return values.bytes() + cols.bytes() + warp_offset.bytes() + maxrows.bytes() +
                rows_in_warp.bytes() + reduction.bytes() + rows_offset_warp.bytes() + fwd.bytes() +
                inv.bytes() + slen.bytes() + slot_map.bytes() + src_map.bytes() + cols16.bytes() + col_base.bytes() +
-               lane_grp.bytes() + ngrp.bytes() + goff.bytes() + gcols.bytes() + gcols16.bytes();
+               lane_grp.bytes() + ngrp.bytes() + goff.bytes() + gcols.bytes() + gcols16.bytes() +
+               col_shift.bytes();
     }
 };
 

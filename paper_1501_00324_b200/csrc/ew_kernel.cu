@@ -150,8 +150,10 @@ std::unique_ptr<HostPipeline> build_pipeline(const KernelData& k, cudaStream_t s
     std::vector<int32_t> fwd(n), mxc(n);
     {
         DevBuf<int32_t> d(n);
-        row_maxcol_kernel<<<grid_for(n), kBlock, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.slen.get(),
-                                                         l.ws_log2, n, d.get());
+        Scratch<int32_t> full(l.cols_full ? 0 : l.nslots, s);  // a dropped int32 slab, decoded for the plan
+        if (!l.cols_full) decode_columns(l, full.get(), s);
+        row_maxcol_kernel<<<grid_for(n), kBlock, 0, s>>>(l.cols_full ? l.cols.get() : full.get(),
+                                                         l.warp_offset.get(), l.slen.get(), l.ws_log2, n, d.get());
         launched("row_maxcol_kernel");
         EW_CUDA_CHECK(cudaMemcpyAsync(mxc.data(), d.get(), n * 4, cudaMemcpyDeviceToHost, s));
         EW_CUDA_CHECK(cudaMemcpyAsync(fwd.data(), l.fwd.get(), n * 4, cudaMemcpyDeviceToHost, s));

@@ -642,6 +642,150 @@ int32_t head_mx() {
     return v;
 }
 
+// ---- the int32 column slab of compact / grouped layouts ---------------------
+struct ColForms {
+    const int64_t* woff;
+    const int32_t* maxrows;
+    const int32_t* rows_in_warp;
+    const int32_t* cols;       // full slab, or the wide warps' slabs (col_shift)
+    const int64_t* col_shift;  // nullptr: cols is the full slab (or empty)
+    const uint16_t* cols16;
+    const int32_t* col_base;   // compact
+    const uint8_t* lane_grp;   // grouped
+    const uint8_t* ngrp;
+    const int64_t* goff;
+    const int32_t* gcols;
+    const uint16_t* gcols16;
+    int32_t ws, ws_log2;
+    int64_t nwarps;
+    int compact, grouped, full;
+};
+
+// The int32 column of each stored slot from the form the kernels read (one
+// hardware warp per layout warp, lanes striding its slots): the wide warps'
+// own slab, the 16-bit offsets (0xFFFF = padding = column 0), or the grouped
+// lists; lanes past the warp's rows are padding (column 0) as in fill_kernel.
+__global__ void decode_cols_kernel(ColForms f, int32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = gw; w < f.nwarps; w += nhw) {
+        const int64_t n = int64_t(f.maxrows[w]) * f.ws, off = f.woff[w];
+        const int32_t nr = f.rows_in_warp[w];
+        const int32_t b = f.compact ? f.col_base[w] : 0;
+        for (int64_t i = lane; i < n; i += 32) {
+            const int32_t l = static_cast<int32_t>(i & (f.ws - 1));
+            const int64_t j = i >> f.ws_log2;
+            int32_t c;
+            if (f.full) {
+                c = f.cols[off + i];
+            } else if (f.compact && b < 0) {
+                c = f.cols[f.col_shift[w] + off + i];
+            } else if (l >= nr) {
+                c = 0;
+            } else if (f.grouped) {
+                const int64_t g = f.goff[w] + j * f.ngrp[w] + f.lane_grp[w * f.ws + l];
+                if (f.compact) {
+                    const uint16_t d = f.gcols16[g];
+                    c = d == 0xFFFFu ? 0 : b + static_cast<int32_t>(d);
+                } else {
+                    c = f.gcols[g];
+                }
+            } else {
+                const uint16_t d = f.cols16[off + i];
+                c = d == 0xFFFFu ? 0 : b + static_cast<int32_t>(d);
+            }
+            out[off + i] = c;
+        }
+    }
+}
+
+// Copies each wide warp's int32 slab to its place in the reduced slab.
+__global__ void wide_copy_kernel(const int32_t* __restrict__ cols, const int64_t* __restrict__ woff,
+                                 const int32_t* __restrict__ maxrows, const int32_t* __restrict__ base,
+                                 const int64_t* __restrict__ shift, int32_t ws, int64_t nwarps,
+                                 int32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nhw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    for (int64_t w = gw; w < nwarps; w += nhw) {
+        if (base[w] >= 0) continue;
+        const int64_t n = int64_t(maxrows[w]) * ws, off = woff[w];
+        for (int64_t i = lane; i < n; i += 32) out[shift[w] + off + i] = cols[off + i];
+    }
+}
+
+__global__ void wide_size_kernel(const int32_t* __restrict__ maxrows, const int32_t* __restrict__ base,
+                                 int32_t ws, int64_t nwarps, int64_t* __restrict__ size) {
+    const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (w < nwarps) size[w] = base[w] < 0 ? int64_t(maxrows[w]) * ws : 0;
+}
+
+__global__ void shift_kernel(const int64_t* __restrict__ woff, int64_t nwarps, int64_t* __restrict__ shift) {
+    const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (w < nwarps) shift[w] -= woff[w];  // wide offset - slab offset
+}
+
+void decode_columns(const LayoutData& l, int32_t* out, cudaStream_t s) {
+    if (l.nslots == 0) return;
+    EW_CUDA_CHECK(cudaMemsetAsync(out, 0, l.nslots * sizeof(int32_t), s));  // alignment gaps
+    ColForms f{l.warp_offset.get(), l.maxrows.get(), l.rows_in_warp.get(), l.cols.get(), l.col_shift.get(),
+               l.cols16.get(), l.col_base.get(), l.lane_grp.get(), l.ngrp.get(), l.goff.get(), l.gcols.get(),
+               l.gcols16.get(), l.ws, l.ws_log2, l.nwarps, l.compact, l.grouped, l.cols_full ? 1 : 0};
+    if (l.nwarps) {
+        decode_cols_kernel<<<fill_grid(l.nwarps), 256, 0, s>>>(f, out);
+        launched("decode_cols_kernel");
+    }
+}
+
+void restore_columns(LayoutData& l, cudaStream_t s) {
+    if (l.cols_full) return;
+    DevBuf<int32_t> full(l.nslots);
+    decode_columns(l, full.get(), s);
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    l.cols = std::move(full);
+    l.col_shift.release();
+    l.cols_full = true;
+}
+
+// Drops the int32 slab the kernels of a compact or grouped layout no longer
+// read (config 2: 4 of its 13.3 bytes per slot; config 5 whole, grouped
+// int32: 4 of 13.5): a compact layout keeps its wide warps' columns only, a
+// grouped int32 one none, unless the SpMV form chosen for it (the
+// cooperative K1) streams the int32 slab. Export, the host-buffer pipeline's
+// plan and the split-x K1 decode or restore it (decode_columns).
+static void shrink_columns(LayoutData& l, cudaStream_t s) {
+    static const bool keep = [] {
+        const char* e = std::getenv("EW_KEEP_INT32_COLS");  // A/B runs
+        return e && e[0] == '1';
+    }();
+    if (keep || !l.cols_full || !(l.compact || l.grouped) || l.nwarps == 0 || spmv_reads_int32(l)) return;
+    if (!l.compact) {  // grouped int32: the kernels read gcols
+        l.cols.release();
+        l.cols_full = false;
+        return;
+    }
+    const int64_t nw = l.nwarps;
+    Scratch<int64_t> size(nw, s);
+    wide_size_kernel<<<grid_for(nw), kBlock, 0, s>>>(l.maxrows.get(), l.col_base.get(), l.ws, nw, size.get());
+    launched("wide_size_kernel");
+    DevBuf<int64_t> shift(nw);
+    exclusive_scan_i64(size.get(), shift.get(), nw, s);
+    const int64_t total = read_scalar(shift.get() + nw - 1, s) + read_scalar(size.get() + nw - 1, s);
+    shift_kernel<<<grid_for(nw), kBlock, 0, s>>>(l.warp_offset.get(), nw, shift.get());
+    launched("shift_kernel");
+    DevBuf<int32_t> wide(total);
+    if (total) {
+        wide_copy_kernel<<<fill_grid(nw), 256, 0, s>>>(l.cols.get(), l.warp_offset.get(), l.maxrows.get(),
+                                                         l.col_base.get(), shift.get(), l.ws, nw, wide.get());
+        launched("wide_copy_kernel");
+    }
+    EW_CUDA_CHECK(cudaStreamSynchronize(s));
+    l.cols = std::move(wide);
+    l.col_shift = std::move(shift);
+    l.cols_full = false;
+}
+
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
                                          int64_t threshold, bool sort_rows, bool row_major,
                                          cudaStream_t s) {
@@ -792,6 +936,7 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
     if (kind == EW_LAYOUT_K1 && !l.row_major && nw) {
         compact_layout(l, s);
         group_layout(l, s);
+        shrink_columns(l, s);
     }
     EW_CUDA_CHECK(cudaStreamSynchronize(s));
     return L;

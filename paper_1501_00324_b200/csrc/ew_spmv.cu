@@ -81,7 +81,13 @@ struct K1Args {
     const int32_t* gcols;
     const uint16_t* gcols16;
     int64_t row_lo;  // k1_kernel (!INDIRECT): thread i runs sorted row row_lo + i (the tail of a head split)
+    const int64_t* col_shift;  // shrunk compact layouts: wide warp w's int32 columns at cols + col_shift[w]
 };
+
+// The int32 columns of (wide) layout warp w, indexed by slot.
+__device__ __forceinline__ const int32_t* wide_cols(const K1Args& a, int64_t w) {
+    return a.col_shift ? a.cols + a.col_shift[w] : a.cols;
+}
 
 __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p, uint64_t pol) {
     uint16_t v;
@@ -267,7 +273,7 @@ __device__ __forceinline__ double k1_row_grouped(const K1Args& a, int64_t w, int
     };
     if (COMPACT) {
         const int32_t base = a.col_base[w];
-        if (base < 0) return lane_sum(a.values, a.cols, a.x, s, a.ws, mx, pol);  // a wide warp: own int32 columns
+        if (base < 0) return lane_sum(a.values, wide_cols(a, w), a.x, s, a.ws, mx, pol);  // a wide warp: own int32 columns
         const uint16_t* g16 = a.gcols16;
         return lane_sum_gx(a.values, [g16, base](int64_t i, uint64_t pl) {
             const uint16_t d = ld_stream(g16 + i, pl);
@@ -297,6 +303,7 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
                 return v;
             }, s, step, mx, pol);
         }
+        return lane_sum(a.values, wide_cols(a, w), a.x, s, step, mx, pol);
     }
     return lane_sum(a.values, a.cols, a.x, s, step, mx, pol);
 }
@@ -434,7 +441,7 @@ __global__ void __launch_bounds__(32 * H, H == 8 ? EW_COOP8_MINB : (H == 4 ? EW_
                         const uint16_t d = ld_stream(a.cols16 + s0 + u * 32, pol);
                         col[u] = d == 0xFFFFu ? 0 : base + static_cast<int32_t>(d);
                     } else {
-                        col[u] = ld_stream(a.cols + s0 + u * 32, pol);
+                        col[u] = ld_stream((COMPACT ? wide_cols(a, w) : a.cols) + s0 + u * 32, pol);
                     }
                 }
             }
@@ -989,6 +996,7 @@ bool layout_spmv_dot(const LayoutData& l, const double* x, double* y, bool scatt
              l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
              l.cols16.get(), l.col_base.get(), nullptr, 0, l.lane_grp.get(), l.ngrp.get(), l.goff.get(),
              l.gcols.get(), l.gcols16.get()};
+    a.col_shift = l.col_shift.get();
     const unsigned grid = grid_for(l.nrows);
     if (cg::dot_partials(grid) > sink.capacity) return false;
     const bool c = l.compact != 0;
@@ -1040,6 +1048,7 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                  l.fwd.get(), x, y, done, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
                  l.cols16.get(), l.col_base.get(), nullptr, 0, l.lane_grp.get(), l.ngrp.get(), l.goff.get(),
                  l.gcols.get(), l.gcols16.get()};
+    a.col_shift = l.col_shift.get();
         const bool rm = l.row_major != 0, sf = streams(l), c = l.compact != 0;
         if (const int h = coop_warps(l)) {
             // EW_K1_BULK=1: the bulk-copy staging form (A/B; needs the
@@ -1120,9 +1129,15 @@ void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, c
     if (nidx == 0 || l.nrows == 0) return;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, nullptr, 0,
-             l.cols16.get(), l.col_base.get(), widx, nidx};
+             l.cols16.get(), l.col_base.get(), widx, nidx, l.lane_grp.get(), l.ngrp.get(), l.goff.get(),
+             l.gcols.get(), l.gcols16.get()};
+    a.col_shift = l.col_shift.get();
     const int64_t threads = nidx << l.ws_log2;
-    if (l.compact)
+    if (l.grouped && l.compact)
+        launch_pdl(k1_kernel<true, true, false, false, true, true, true>, grid_for(threads, 64), 64, s, a);
+    else if (l.grouped)
+        launch_pdl(k1_kernel<true, true, false, false, false, true, true>, grid_for(threads), kBlock, s, a);
+    else if (l.compact)
         launch_pdl(k1_kernel<true, true, false, false, true, true>, grid_for(threads, 64), 64, s, a);
     else
         launch_pdl(k1_kernel<true, true, false, false, false, true>, grid_for(threads), kBlock, s, a);
@@ -1132,6 +1147,7 @@ void layout_spmv_warps(const LayoutData& l, const int32_t* widx, int64_t nidx, c
 void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, int64_t nown, double* y,
                        cudaStream_t s) {
     require(l.kind == EW_LAYOUT_K1 && !l.row_major, "split-x SpMV: K1 column-major layouts only");
+    require(l.cols_full, "split-x SpMV: the layout's int32 columns were dropped (restore_columns)");
     if (l.nrows == 0) return;
     K1Args a{l.values.get(), l.cols.get(), l.warp_offset.get(), l.maxrows.get(), l.slen.get(),
              l.fwd.get(), x, y, nullptr, l.nrows, l.n_active, l.ws, l.ws_log2, xg, static_cast<int32_t>(nown),
@@ -1147,6 +1163,13 @@ void layout_spmv_split(const LayoutData& l, const double* x, const double* xg, i
         launch_pdl(k1_kernel<false, true, false, true>, grid_for(a.nrows), kBlock, s, a);
     }
     launched("k1_kernel");
+}
+
+bool spmv_reads_int32(const LayoutData& l) {
+    if (l.kind != EW_LAYOUT_K1 || l.row_major) return true;
+    if (l.compact) return false;  // 16-bit forms; wide warps through col_shift
+    if (!l.grouped) return true;
+    return coop_warps(l) != 0;  // the cooperative K1 runs before the grouped form
 }
 
 // Shared-memory opt-in of k1_long_kernel on the current device (a layout

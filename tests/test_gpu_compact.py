@@ -52,9 +52,13 @@ def dev(ew, m):
 
 
 def compact_in_use(k):
-    """Most slots stream 16-bit columns (ew_kernel_info.narrow_slots)."""
+    """Most slots stream 16-bit columns (ew_kernel_info.narrow_slots), and
+    the layout holds no int32 columns for them (shrink_columns: 8 B of value
+    + 2 B of offset per narrow slot, int32 only for the wide warps)."""
     i = k.info()
-    return i.narrow_slots * 2 > i.stored_slots and i.device_bytes >= 14 * i.narrow_slots
+    return (i.narrow_slots * 2 > i.stored_slots and i.device_bytes >= 10 * i.narrow_slots
+            and i.col_stream_bytes == 2 * i.narrow_slots + 4 * (i.stored_slots - i.narrow_slots)
+            and i.device_bytes < 12 * i.stored_slots + 40 * i.nrows)
 
 
 @pytest.mark.parametrize("kid", ["k1", "k1r", "k1rs"])
