@@ -748,11 +748,12 @@ void restore_columns(LayoutData& l, cudaStream_t s) {
     l.cols_full = true;
 }
 
-// Drops the int32 slab the kernels of a compact or grouped layout no longer
-// read (config 2: 4 of its 13.3 bytes per slot; config 5 whole, grouped
-// int32: 4 of 13.5): a compact layout keeps its wide warps' columns only, a
-// grouped int32 one none, unless the SpMV form chosen for it (the
-// cooperative K1) streams the int32 slab. Export, the host-buffer pipeline's
+// Drops the column slabs the kernels of a compact or grouped layout no
+// longer read: a compact layout keeps int32 columns for its wide warps only
+// (and, grouped, no per-slot 16-bit offsets either: config 2 14.7 -> ~8.8
+// bytes per slot), a grouped int32 one no int32 slab (config 5 whole: 18 GB),
+// unless the SpMV form chosen for it (the cooperative K1) streams the int32
+// slab. Export, the host-buffer pipeline's
 // plan and the split-x K1 decode or restore it (decode_columns).
 static void shrink_columns(LayoutData& l, cudaStream_t s) {
     static const bool keep = [] {
@@ -784,6 +785,7 @@ static void shrink_columns(LayoutData& l, cudaStream_t s) {
     l.cols = std::move(wide);
     l.col_shift = std::move(shift);
     l.cols_full = false;
+    if (l.grouped) l.cols16.release();  // the grouped lists replace the per-slot offsets too
 }
 
 std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_warp_config& cfg,
