@@ -185,6 +185,7 @@ void k1_long_setup();  // ew_spmv.cu: k1_long_kernel's shared-memory opt-in (cur
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    std::mutex mu;  // one fork ... join sequence at a time (callers on several host threads)
     SideStream() {
         EW_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         EW_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));

@@ -1073,7 +1073,8 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
             // k1_long_kernel (ncu: head 62 us, tail 39 us, concurrent);
             // circuit keeps the cooperative K1 everywhere (773 vs 604 GB/s
             // effective split)
-            const SideStream& ss = *l.side;
+            SideStream& ss = *l.side;
+            std::lock_guard<std::mutex> lock(ss.mu);
             EW_CUDA_CHECK(cudaEventRecord(ss.fork, s));
             EW_CUDA_CHECK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
             static const bool coop_head = [] {  // A/B: the cooperative K1 (H = 8) for the head
