@@ -313,6 +313,13 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
 #ifndef EW_K1C_MINB
 #define EW_K1C_MINB 5
 #endif
+// grouped int32 layouts (config 5): plain and grid-stride forms
+#ifndef EW_K1G_STREAM_MINB
+#define EW_K1G_STREAM_MINB 8
+#endif
+#ifndef EW_K1G_MINB
+#define EW_K1G_MINB 8
+#endif
 #ifndef EW_K1P_MINB
 #define EW_K1P_MINB 8
 #endif
@@ -321,7 +328,8 @@ __device__ __forceinline__ double k1_row(const K1Args& a, int64_t w, int64_t s, 
 // whole-layout launch, so the same row sums.
 template <bool SORTED, bool SCATTER, bool ROW_MAJOR, bool SPLIT_X = false, bool COMPACT = false,
           bool INDIRECT = false, bool GROUPED = false>
-__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_kernel(K1Args a) {
+__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : (GROUPED ? EW_K1G_MINB : EW_K1P_MINB))
+    k1_kernel(K1Args a) {
     pdl_wait();
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (!INDIRECT) p += a.row_lo;
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_k
 // plain form instead: with the narrower column loads the stream form spills
 // more (221 us cold on config 2) and the plain one wins (158.0 us vs 163.6).
 template <bool SORTED, bool SCATTER, bool SPLIT_X = false, bool GROUPED = false>
-__global__ void __launch_bounds__(256, 8) k1_stream_kernel(K1Args a) {
+__global__ void __launch_bounds__(256, GROUPED ? EW_K1G_STREAM_MINB : 8) k1_stream_kernel(K1Args a) {
     pdl_wait();
     if (a.done && *a.done) return;
     const uint64_t pol = evict_first_policy();
@@ -752,7 +760,8 @@ inline bool streams(const LayoutData& l) {
 // cg::dot_final_kernel sums the partials and decides. The CTA only stores
 // its partial: no fence or atomic holds it past its last row.
 template <bool SORTED, bool SCATTER, bool COMPACT = false, bool GROUPED = false>
-__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_dot_kernel(K1Args a, double* __restrict__ partials) {
+__global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : (GROUPED ? EW_K1G_MINB : EW_K1P_MINB))
+    k1_dot_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -782,7 +791,8 @@ __global__ void __launch_bounds__(256, COMPACT ? EW_K1C_MINB : EW_K1P_MINB) k1_d
 
 // k1_dot_kernel in the grid-stride form of k1_stream_kernel (large long-row layouts).
 template <bool SORTED, bool SCATTER, bool GROUPED = false>
-__global__ void __launch_bounds__(256, 8) k1_dot_stream_kernel(K1Args a, double* __restrict__ partials) {
+__global__ void __launch_bounds__(256, GROUPED ? EW_K1G_STREAM_MINB : 8)
+    k1_dot_stream_kernel(K1Args a, double* __restrict__ partials) {
     pdl_wait();
     if (a.done && *a.done) return;  // uniform across the grid
     const uint64_t pol = evict_first_policy();
