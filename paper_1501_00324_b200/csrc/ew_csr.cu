@@ -51,11 +51,18 @@ void load_all_kernels() {
     auto kernel_count = reinterpret_cast<KernelCount>(entry("cuLibraryGetKernelCount"));
     auto enumerate = reinterpret_cast<Enumerate>(entry("cuLibraryEnumerateKernels"));
     auto get_function = reinterpret_cast<GetFunction>(entry("cuKernelGetFunction"));
-    require(get_library && kernel_count && enumerate && get_function,
-            "load_all_kernels: the driver lacks cuLibraryEnumerateKernels (CUDA >= 12.5)");
-    for (const void* anchor : {kernel_anchor_assembly(), kernel_anchor_dist(), kernel_anchor_formats(),
-                               kernel_anchor_kernel(), kernel_anchor_layout(), kernel_anchor_order(),
-                               kernel_anchor_spmv(), kernel_anchor_csr()}) {
+    const void* anchors[] = {kernel_anchor_assembly(), kernel_anchor_dist(), kernel_anchor_formats(),
+                             kernel_anchor_kernel(), kernel_anchor_layout(), kernel_anchor_order(),
+                             kernel_anchor_spmv(), kernel_anchor_csr()};
+    if (!(get_library && kernel_count && enumerate && get_function)) {
+        // a driver before CUDA 12.5: load what can be named (the anchors);
+        // CUDA_MODULE_LOADING=EAGER in the environment covers the rest
+        cudaFuncAttributes fa;
+        for (const void* anchor : anchors) EW_CUDA_CHECK(cudaFuncGetAttributes(&fa, anchor));
+        done_mask |= bit;
+        return;
+    }
+    for (const void* anchor : anchors) {
         cudaKernel_t k = nullptr;
         EW_CUDA_CHECK(cudaGetKernel(&k, anchor));
         CUlibrary lib = nullptr;
