@@ -916,7 +916,8 @@ def run_suite(args):
                                               for k2, v2 in spec.items()}},
                "gen_s": round(time.time() - t, 1)}
         for kid in kernels:
-            thresholds = [0] if not kid.startswith("k2") else sorted({4, 8, 16, 32, max(1, int(lens.max()))})
+            sweep = [int(t) for t in args.suite_thresholds.split(",")] if args.suite_thresholds else [4, 8, 12, 16, 20, 24, 32]
+            thresholds = [0] if not kid.startswith("k2") else sorted(set(sweep) | {max(1, int(lens.max()))})
             best = None
             for th in thresholds:
                 try:
@@ -1089,6 +1090,7 @@ def main():
     p.add_argument("--alpha-reps", type=int, default=9)
     p.add_argument("--suite-iters", type=int, default=5)
     p.add_argument("--suite-only", default="", help="comma-separated Table 2 names (suite workload)")
+    p.add_argument("--suite-thresholds", default="", help="K2 thresholds to sweep (suite; default 4,8,12,16,20,24,32 + maxrow)")
     p.add_argument("--config", default=None)
     p.add_argument("--kernel", default=None)
     p.add_argument("--threshold", type=int, default=0)
