@@ -237,24 +237,31 @@ __device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t e, uint64
     }
 }
 
-// Pack and transfer in one kernel: the owned values each destination needs
-// are stored straight into its ghost tail (peer stores over NVLink), then the
-// last CTA raises the destination's halo flag (release, system scope).
-// Before writing, every destination must have consumed the previous epoch
+// Before a push, every destination must have consumed the previous epoch
 // (its ack in this rank's mailbox); with write_acks this rank first acks the
 // previous epoch to its own sources (its boundary rows of that epoch are
-// done: this kernel is stream-ordered after them).
-__global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int32_t* __restrict__ idx,
-                            const double* __restrict__ src, int which, const uint64_t* epochs, uint64_t* const* mboxes,
-                            int me, int G, int write_acks, const int32_t* __restrict__ srcs, int nsrc,
-                            unsigned* ctr, int64_t total) {
+// done: this kernel is stream-ordered after them). One CTA spins, not the
+// push grid: partitions sharing a GPU (or a GPU shared with other work)
+// keep their SM slots for the kernels that produce the awaited acks.
+__global__ void ack_exchange_kernel(const PushDesc* __restrict__ d, int ndesc, const uint64_t* epochs,
+                                    uint64_t* const* mboxes, int me, int G, int write_acks,
+                                    const int32_t* __restrict__ srcs, int nsrc) {
     uint64_t* mine = mboxes[me];
     const uint64_t epoch = epochs[0] + 1;  // this exchange (halo_wait_kernel advances the counter)
-    if (write_acks && blockIdx.x == 0)
+    if (write_acks)
         for (int i = threadIdx.x; i < nsrc; i += blockDim.x) st_release_sys(mboxes[srcs[i]] + Mbox::ack(G, me), epoch - 1);
     for (int i = threadIdx.x; i < ndesc; i += blockDim.x)
         spin_until(mine + Mbox::ack(G, d[i].peer), epoch - 1, mine + Mbox::err(G));
-    __syncthreads();
+}
+
+// Pack and transfer in one kernel (after ack_exchange_kernel on the same
+// stream): the owned values each destination needs are stored straight into
+// its ghost tail (peer stores over NVLink), then the last CTA raises the
+// destination's halo flag (release, system scope).
+__global__ void push_kernel(const PushDesc* __restrict__ d, int ndesc, const int32_t* __restrict__ idx,
+                            const double* __restrict__ src, int which, const uint64_t* epochs, uint64_t* const* mboxes,
+                            int me, unsigned* ctr, int64_t total) {
+    const uint64_t epoch = epochs[0] + 1;  // this exchange (halo_wait_kernel advances the counter)
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
         int i = 0;
         while (k >= d[i].off + d[i].cnt) ++i;
@@ -652,9 +659,11 @@ void peer_push(DistData& D, int which, DevBuf<double> DistPart::*ext, cudaStream
         if (!total && (!D.ipc || !P->nsrc)) continue;
         const unsigned grid = std::max<unsigned>(1, std::min<unsigned>(grid_for(total), 148 * 4));
         const double* from = src ? (*src)[i] : ((*P).*ext).get();
+        ack_exchange_kernel<<<1, 32, 0, s>>>(P->descs.get(), P->ndesc, P->epochs.get(), P->mboxes.get(), P->part, G,
+                                             D.ipc ? 1 : 0, P->srcs.get(), P->nsrc);
+        launched("ack_exchange_kernel");
         push_kernel<<<grid, kBlock, 0, s>>>(P->descs.get(), P->ndesc, P->send_idx.get(), from, which, P->epochs.get(),
-                                            P->mboxes.get(), P->part, G, D.ipc ? 1 : 0, P->srcs.get(), P->nsrc,
-                                            P->push_ctr.get(), total);
+                                            P->mboxes.get(), P->part, P->push_ctr.get(), total);
         launched("push_kernel");
     }
 }
