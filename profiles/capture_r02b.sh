@@ -16,3 +16,10 @@ ncu --metrics $M --clock-control none -k regex:"k1_dot|dot_final|update_kernel|p
 ncu --set full --import-source on --clock-control none -k regex:"k1_(stream_)?kernel" -s 5 -c 1 -o $O/r02b_k1_c2_grouped_full \
     python bench.py --steps 10 --warmup 3 --no-cpu-baseline --cg-steps 0 > /dev/null 2>&1
 ls -la $O
+# 4. (later in round 2b) CG iteration kernels, config 4 locality order, after the update / p prefetch
+ncu --metrics $M --clock-control none -k regex:"k1_dot|dot_final|update_kernel|p_kernel" -s 80 -c 40 --csv \
+    --log-file $O/r02b_ncu_cg_c4_locality_launches.csv \
+    python bench.py --workload cg --steps 1 --warmup 3 --iterations 50 --both-orders 0 --no-cpu-baseline > /dev/null 2>&1
+# 5. K2 on accelerator in 128-thread CTAs at T = 20 (full sections)
+ncu --set full --import-source on --clock-control none -k regex:k2_kernel -c 1 -o $O/r02b_k2_accel_full \
+    python profiles/suite_once.py accelerator k2:20 > /dev/null 2>&1
