@@ -348,3 +348,28 @@ def test_k1_head_split_power_law(ew, F, kid):
     assert same(k.apply(x), F.apply(kid, m, x))
     x[0] = np.nan  # padding terms 0 * x[0] as the reference executes them
     assert same(k.apply(x), F.apply(kid, m, x))
+
+
+def _table2_names():
+    from paper_1501_00324_b200 import workloads as W
+
+    return [t[0] for t in W.TABLE2]
+
+
+@pytest.mark.parametrize("name", _table2_names())
+def test_table2_size_kernels_bitwise(ew, F, name):
+    """Config 3 at Table 2 sizes (the suite bench's matrices), every form
+    the layouts select there -- the cooperative K1, the head split
+    (webbase), 16-bit / grouped columns past 64 MB, K2 in 128-thread CTAs
+    at the suite's thresholds -- bitwise the compiled reference."""
+    from oracle.oracle import Csr
+    from paper_1501_00324_b200 import workloads as W
+
+    n, nc, ro, ci, v = W.table2_matrix(name)
+    m = Csr.make(n, nc, ro, ci, v)
+    x = F.random_vector(nc, 5)
+    a = dev_csr(ew, m)
+    for kid in ("k1", "k1rs"):
+        assert same(ew.Kernel(kid, a).apply(x), F.apply(kid, m, x)), kid
+    for t in (16, 32):
+        assert same(ew.Kernel("k2", a, threshold=t).apply(x), F.apply("k2", m, x, threshold=t)), t
