@@ -910,7 +910,11 @@ std::shared_ptr<LayoutData> build_layout(const CsrData& m, int kind, const ew_wa
                 if (read_scalar(l.maxrows.get() + mid, s) > hm) lo = mid + 1;
                 else hi = mid;
             }
-            l.head_warps = lo;
+            // at most four 1024-thread CTAs per SM of head: the long-row
+            // kernel spends a whole CTA on each layout warp, which pays for
+            // the few longest rows, not for a fat band of moderately long
+            // ones (the plain K1 keeps those; any split point is valid)
+            l.head_warps = std::min<int64_t>(lo, 148 * 4);
             if (lo > 0) {
                 l.side = std::make_shared<SideStream>();
                 k1_long_setup();

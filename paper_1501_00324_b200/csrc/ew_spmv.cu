@@ -496,7 +496,9 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <bool SCATTER>
+// FORM: the column form the layout keeps -- 0 int32, 1 16-bit offsets (wide
+// warps: their int32 columns), 2 grouped int32 lists, 3 grouped 16-bit.
+template <bool SCATTER, int FORM>
 __global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
     extern __shared__ double prod[];  // [2][kLongChunk][32]
     if (a.done && *a.done) return;    // uniform across the grid
@@ -505,6 +507,11 @@ __global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
     const int64_t p = (w << 5) + lane;
     const int32_t mx = __ldg(a.maxrows + w);
     const int64_t wo = __ldg(a.woff + w);
+    constexpr bool kCompact = FORM == 1 || FORM == 3, kGrouped = FORM >= 2;
+    const int32_t base = kCompact ? __ldg(a.col_base + w) : 0;
+    const int32_t* wc = kCompact ? wide_cols(a, w) : a.cols;
+    const int64_t g0 = kGrouped && p < a.nrows ? a.goff[w] + a.lane_grp[p] : 0;
+    const int32_t ng = kGrouped ? a.ngrp[w] : 0;
     const int nchunks = (mx + kLongChunk - 1) / kLongChunk;
     if (warp == 0) {
         const int64_t target = SCATTER && p < a.nrows ? a.fwd[p] : p;
@@ -534,8 +541,20 @@ __global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
                 int32_t col[8];
                 double v[8], xv[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (u < cnt) col[u] = ld_stream(a.cols + s0 + u * 32, pol);
+                for (int u = 0; u < 8; ++u) {
+                    if (u >= cnt) continue;
+                    const int64_t sl = s0 + u * 32;
+                    if (FORM == 0 || (kCompact && base < 0)) {
+                        col[u] = ld_stream(wc + sl, pol);
+                    } else if (FORM == 2) {
+                        col[u] = p < a.nrows ? ld_stream(a.gcols + g0 + int64_t(j0 + u) * ng, pol) : 0;
+                    } else {
+                        const uint16_t d = FORM == 1 ? ld_stream(a.cols16 + sl, pol)
+                                           : p < a.nrows ? ld_stream(a.gcols16 + g0 + int64_t(j0 + u) * ng, pol)
+                                                         : uint16_t(0xFFFF);
+                        col[u] = d == 0xFFFFu ? 0 : base + static_cast<int32_t>(d);
+                    }
+                }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
                     if (u < cnt) v[u] = ld_stream(a.values + s0 + u * 32, pol);
@@ -556,8 +575,12 @@ __global__ void __launch_bounds__(1024, 1) k1_long_kernel(K1Args a) {
 }
 
 template <bool SCATTER>
-void launch_k1_long(const K1Args& a, int64_t nwarps, cudaStream_t s) {
-    k1_long_kernel<SCATTER><<<static_cast<unsigned>(nwarps), 1024, kLongSmem, s>>>(a);
+void launch_k1_long(const K1Args& a, int64_t nwarps, int form, cudaStream_t s) {
+    const unsigned g = static_cast<unsigned>(nwarps);
+    if (form == 0) k1_long_kernel<SCATTER, 0><<<g, 1024, kLongSmem, s>>>(a);
+    else if (form == 1) k1_long_kernel<SCATTER, 1><<<g, 1024, kLongSmem, s>>>(a);
+    else if (form == 2) k1_long_kernel<SCATTER, 2><<<g, 1024, kLongSmem, s>>>(a);
+    else k1_long_kernel<SCATTER, 3><<<g, 1024, kLongSmem, s>>>(a);
     EW_CUDA_CHECK(cudaGetLastError());
     launched("k1_long_kernel");
 }
@@ -1073,7 +1096,7 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                 scatter ? launch_k1_coop<true>(a, l.nwarps, h, c, s) : launch_k1_coop<false>(a, l.nwarps, h, c, s);
             return;
         }
-        if (l.head_warps > 0 && !c && !l.grouped && !rm && !l.imported) {
+        if (l.head_warps > 0 && !rm && !l.imported) {
             // power-law rows, too many for the cooperative K1 everywhere
             // (webbase: 1M rows, one of 4,700 entries): the head warps (rows
             // over head_mx() entries) run the cooperative K1 on the side
@@ -1082,7 +1105,9 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
             // with k1_coop_kernel (H = 8) as the head, 76 us with
             // k1_long_kernel (ncu: head 62 us, tail 39 us, concurrent);
             // circuit keeps the cooperative K1 everywhere (773 vs 604 GB/s
-            // effective split)
+            // effective split). Any column form (16-bit / grouped layouts
+            // over 64 MB with a few long rows: the head reads the kept form)
+            const int form = (l.grouped ? 2 : 0) + (c ? 1 : 0);
             SideStream& ss = *l.side;
             std::lock_guard<std::mutex> lock(ss.mu);
             EW_CUDA_CHECK(cudaEventRecord(ss.fork, s));
@@ -1091,18 +1116,28 @@ void layout_spmv(const LayoutData& l, const double* x, double* y, bool scatter, 
                 const char* e = std::getenv("EW_K1_HEAD_COOP");
                 return e && e[0] == '1';
             }();
-            if (coop_head)
+            if (coop_head && form == 0)
                 scatter ? launch_k1_coop<true>(a, l.head_warps, 8, false, ss.s)
                         : launch_k1_coop<false>(a, l.head_warps, 8, false, ss.s);
             else
-                scatter ? launch_k1_long<true>(a, l.head_warps, ss.s) : launch_k1_long<false>(a, l.head_warps, ss.s);
+                scatter ? launch_k1_long<true>(a, l.head_warps, form, ss.s)
+                        : launch_k1_long<false>(a, l.head_warps, form, ss.s);
             const int64_t lo = l.head_warps * 32;
-            if (lo < l.nrows) {
+            if (lo < l.nrows) {  // the tail: the plain form of the layout's columns (row_lo offset)
                 K1Args t = a;
                 t.row_lo = lo;
-                const unsigned g = grid_for(l.nrows - lo);
-                scatter ? launch_pdl(k1_kernel<true, true, false>, g, kBlock, s, t)
-                        : launch_pdl(k1_kernel<true, false, false>, g, kBlock, s, t);
+                const int b = c ? 64 : kBlock;
+                const unsigned g = grid_for(l.nrows - lo, b);
+                auto go = [&](auto kernel) { launch_pdl(kernel, g, b, s, t); };
+                if (form == 0) scatter ? go(k1_kernel<true, true, false>) : go(k1_kernel<true, false, false>);
+                else if (form == 1)
+                    scatter ? go(k1_kernel<true, true, false, false, true>) : go(k1_kernel<true, false, false, false, true>);
+                else if (form == 2)
+                    scatter ? go(k1_kernel<true, true, false, false, false, false, true>)
+                            : go(k1_kernel<true, false, false, false, false, false, true>);
+                else
+                    scatter ? go(k1_kernel<true, true, false, false, true, false, true>)
+                            : go(k1_kernel<true, false, false, false, true, false, true>);
                 launched("k1_kernel");
             }
             EW_CUDA_CHECK(cudaEventRecord(ss.join, ss.s));
@@ -1186,10 +1221,16 @@ bool spmv_reads_int32(const LayoutData& l) {
 // Shared-memory opt-in of k1_long_kernel on the current device (a layout
 // with a head split calls this when it is built, outside any capture).
 void k1_long_setup() {
-    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kLongSmem)));
-    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kLongSmem)));
+    const int bytes = static_cast<int>(kLongSmem);
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true, 0>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true, 1>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true, 2>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<true, 3>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false, 0>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false, 1>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false, 2>, attr, bytes));
+    EW_CUDA_CHECK(cudaFuncSetAttribute(k1_long_kernel<false, 3>, attr, bytes));
 }
 
 const void* kernel_anchor_spmv() { return reinterpret_cast<const void*>(&k1_stream_kernel<true, false>); }

@@ -373,3 +373,51 @@ def test_table2_size_kernels_bitwise(ew, F, name):
         assert same(ew.Kernel(kid, a).apply(x), F.apply(kid, m, x)), kid
     for t in (16, 32):
         assert same(ew.Kernel("k2", a, threshold=t).apply(x), F.apply("k2", m, x, threshold=t)), t
+
+
+def _long_head_matrix(grouped):
+    """Over 64 MB of slab with narrow warps (16-bit columns) and a few very
+    long rows: 400k rows of 100 entries plus one of 3,000 (compact), or 150k
+    nodes x 3 unknowns sharing each node's 34 columns plus one node of 3,000
+    (compact + grouped)."""
+    from oracle.oracle import Csr
+
+    if grouped:
+        nodes, per = 150_000, 34
+        nl = np.full(nodes, per, np.int64)
+        nl[5] = 3000
+        n = 3 * nodes
+        lens = np.repeat(nl, 3)
+        node_of = np.repeat(np.arange(nodes, dtype=np.int64), 3)
+    else:
+        n = 400_000
+        lens = np.full(n, 100, np.int64)
+        lens[7] = 3000
+        node_of = np.arange(n, dtype=np.int64)
+    ro = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ro[1:])
+    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
+    j = np.arange(ro[-1]) - np.repeat(ro[:-1], lens)
+    cols = (np.repeat(node_of, lens) * 7 + j * 13) % n
+    cols = np.sort(rows * n + cols) - rows * n
+    vals = np.random.default_rng(2).uniform(0.1, 1.0, ro[-1])
+    return Csr.make(n, n, ro, cols, vals)
+
+
+@pytest.mark.parametrize("grouped", [False, True], ids=["compact", "grouped"])
+def test_k1_head_split_compact_and_grouped(ew, F, grouped):
+    """The head split on layouts over 64 MB (16-bit / grouped columns, int32
+    slab dropped): the long rows' warps through k1_long_kernel reading the
+    kept column form, the rest through the matching plain form -- bitwise
+    the reference K1, non-finite x[0] included."""
+    m = _long_head_matrix(grouped)
+    a = dev_csr(ew, m)
+    k = ew.Kernel("k1", a)
+    i = k.info()
+    assert i.narrow_slots > 0.9 * i.stored_slots
+    if grouped:
+        assert i.col_stream_bytes < 2 * i.stored_slots
+    x = F.random_vector(m.ncols, 9)
+    assert same(k.apply(x), F.apply("k1", m, x))
+    x[0] = np.nan
+    assert same(k.apply(x), F.apply("k1", m, x))
