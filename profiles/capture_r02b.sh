@@ -23,3 +23,6 @@ ncu --metrics $M --clock-control none -k regex:"k1_dot|dot_final|update_kernel|p
 # 5. K2 on accelerator in 128-thread CTAs at T = 20 (full sections)
 ncu --set full --import-source on --clock-control none -k regex:k2_kernel -c 1 -o $O/r02b_k2_accel_full \
     python profiles/suite_once.py accelerator k2:20 > /dev/null 2>&1
+# 6. config 3 suite: one launch of K1 / K1rs / K2 (T 16, 20, 32) per matrix with the round-2b kernels
+ncu --metrics $M --clock-control none -k regex:"k1_|k2_kernel" --csv --log-file $O/r02b_ncu_suite_launches.csv \
+    python profiles/suite_once.py "" k1,k1rs,k2:16,k2:20,k2:32 > /dev/null 2>&1
